@@ -1,0 +1,246 @@
+/*
+ * oracle.c — plain, slow, single-threaded CPU oracle of the Sync-Switch synchronization path.
+ *
+ * TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs; never by the product path. Shares nothing with paper_2104_08364_b200/.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -std=c11 -shared -fPIC oracle.c -lm -o liboracle.so
+ * (-ffp-contract=off: every fused multiply-add is the explicit fmaf()/fma() the text below writes; nothing else
+ * is contracted, so float arithmetic is exactly what is written, in the order written).
+ *
+ * Parity status per function:
+ *   shard layout, lr, Table I, state machine, synth grad, schedule, detector: pinned (tests/test_oracle_*.py).
+ *   softmax toy model: pinned by closed forms (ln C at W=0) and central finite differences.
+ */
+#include "oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Shard layout. P:15 "one needs to divide the model parameters into different shards, each shard managed by one
+ * PS instance"; the method is a TODO in the paper, so SURVEY §8 fixes it: equal contiguous shards padded
+ * to 32 floats (128 B), owner(s) = floor(s*G/S), host(j) = floor(j*G/n). */
+int64_t orc_shard_pad(int64_t P, int32_t S) {
+  int64_t per = (P + S - 1) / S;          /* ceil(P/S) */
+  return ((per + 31) / 32) * 32;          /* round up to 32 floats */
+}
+
+void orc_shard_offsets(int64_t P, int32_t S, int64_t *off) {
+  int64_t pad = orc_shard_pad(P, S);
+  for (int32_t s = 0; s <= S; s++) {
+    int64_t o = (int64_t)s * pad;
+    off[s] = o < P ? o : P;
+  }
+}
+
+int32_t orc_shard_owner(int32_t s, int32_t S, int32_t G) { return (int32_t)(((int64_t)s * G) / S); }
+int32_t orc_worker_host(int32_t j, int32_t n, int32_t G) { return (int32_t)(((int64_t)j * G) / n); }
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Learning rate. P:1600: "learning rate to be 0.1 and decays ... at 32K and 48K steps with scaling factors of 0.1
+ * and 0.01"; factors multiply the base rate, not each other ("not cumulative"); right-continuous. */
+double orc_lr_factor(int64_t version, const int64_t *bounds, const float *factors, int32_t nb) {
+  double f = 1.0;
+  for (int32_t i = 0; i < nb; i++)
+    if (bounds[i] <= version) f = (double)factors[i];
+  return f;
+}
+
+/* P:1473 "eta_BSP = n*eta" (linear scaling rule); "eta_ASP = eta/sqrt(n)" (reading C3: rule 0 = 1/sqrt(n),
+ * rule 1 = 1/n, rule 2 = unscaled). Computed in double, rounded to float once. */
+float orc_lr(float eta, double factor, int32_t proto, int32_t n, int32_t asp_rule) {
+  double scale;
+  if (proto == ORC_BSP) scale = (double)n;
+  else if (asp_rule == 0) scale = 1.0 / sqrt((double)n);
+  else if (asp_rule == 1) scale = 1.0 / (double)n;
+  else scale = 1.0;
+  return (float)((double)eta * factor * scale);
+}
+
+/* Table I: BSP steps = W*s/(B*N); ASP steps = W/B - W*s/B; a decay boundary W_i (in samples) moves to
+ * W_i/B - W*s/B + W*s/(B*N) when it lies after the BSP share, else to W_i/(B*N) (reading C11: the draft's single
+ * formula gives negative boundaries for rows 75-25 and 100-0; the piecewise rule reproduces all 11 rows). */
+int32_t orc_table1(int64_t W, int64_t B, int64_t N, int64_t s_num, int64_t s_den, const int64_t *Wb, int32_t nb,
+                   int64_t *bsp_steps, int64_t *asp_steps, int64_t *bounds_out) {
+  if (W <= 0 || B <= 0 || N <= 0 || s_den <= 0 || s_num < 0 || s_num > s_den) return -1;
+  /* Ws = W*s samples processed under BSP; must be integral, as must the step counts. */
+  if ((W * s_num) % s_den != 0) return -1;
+  int64_t Ws = W * s_num / s_den;
+  if (Ws % (B * N) != 0 || W % B != 0 || Ws % B != 0) return -1;
+  *bsp_steps = Ws / (B * N);
+  *asp_steps = W / B - Ws / B;
+  for (int32_t i = 0; i < nb; i++) {
+    if (Wb[i] % B != 0) return -1;
+    if (Wb[i] <= Ws) {
+      if (Wb[i] % (B * N) != 0) return -1;
+      bounds_out[i] = Wb[i] / (B * N);
+    } else {
+      bounds_out[i] = Wb[i] / B - Ws / B + Ws / (B * N);
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------------------------
+ * The state machine, instantiated for float (parity) and double (identities). */
+#define REAL float
+#define ORC_T orc_f
+#define ORC_FN(x) orcf##x
+#define ORC_FMA fmaf
+#include "oracle_state.inc"
+#undef REAL
+#undef ORC_T
+#undef ORC_FN
+#undef ORC_FMA
+
+#define REAL double
+#define ORC_T orc_d
+#define ORC_FN(x) orcd##x
+#define ORC_FMA fma
+#include "oracle_state.inc"
+#undef REAL
+#undef ORC_T
+#undef ORC_FN
+#undef ORC_FMA
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Synthetic inputs, written from their stated formulas. splitmix64 = Steele/Lea/Flood's finaliser
+ * with the golden-gamma increment. */
+uint64_t orc_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void orc_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *out) {
+  for (int64_t t = 0; t < count; t++) {
+    uint64_t i = (uint64_t)(i0 + t);
+    uint64_t key = ((uint64_t)(uint32_t)j << 56) ^ ((uint64_t)k << 30) ^ i;
+    uint64_t h = orc_splitmix64(seed ^ key);
+    double u = (double)(h >> 40) * (1.0 / 16777216.0);  /* 24-bit integer * 2^-24, exact */
+    out[t] = (float)((u - 0.5) * (1.0 / 64.0));         /* exact in float: 24 significant bits at most */
+  }
+}
+
+/* Arrival schedule (reading C7). Plain event simulation: keep each worker's next push tick; repeatedly take the
+ * smallest (tick, worker); emit push then the same worker's pull. */
+int64_t orc_schedule(int32_t n, const int64_t *period, int64_t jitter, uint64_t seed, int32_t slow_worker,
+                     int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t n_push, int32_t *ev_kind,
+                     int32_t *ev_worker, int64_t *ev_tick) {
+  int64_t *next = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+  int64_t *count = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+  int64_t e = 0;
+  for (int32_t j = 0; j < n; j++) {          /* every worker pulls at t = 0 */
+    ev_kind[e] = 1; ev_worker[e] = j; ev_tick[e] = 0; e++;
+  }
+  for (int32_t j = 0; j < n; j++) {
+    int64_t prev = 0, k = 1;
+    int64_t T = period[j];
+    if (j == slow_worker && prev >= slow_t0 && prev < slow_t1) T *= slow_factor;
+    int64_t d = 0;
+    if (jitter > 0)
+      d = (int64_t)(orc_splitmix64(seed ^ ((uint64_t)(uint32_t)j << 32) ^ (uint64_t)k) % (uint64_t)(2 * jitter + 1)) -
+          jitter;
+    next[j] = prev + T + d;
+  }
+  for (int64_t p = 0; p < n_push; p++) {
+    int32_t best = 0;
+    for (int32_t j = 1; j < n; j++)
+      if (next[j] < next[best]) best = j;      /* ties broken by the lower worker id */
+    int64_t t = next[best];
+    ev_kind[e] = 0; ev_worker[e] = best; ev_tick[e] = t; e++;
+    ev_kind[e] = 1; ev_worker[e] = best; ev_tick[e] = t; e++;
+    count[best] += 1;
+    int64_t k = count[best] + 1;
+    int64_t T = period[best];
+    if (best == slow_worker && t >= slow_t0 && t < slow_t1) T *= slow_factor;
+    int64_t d = 0;
+    if (jitter > 0)
+      d = (int64_t)(orc_splitmix64(seed ^ ((uint64_t)(uint32_t)best << 32) ^ (uint64_t)k) %
+                    (uint64_t)(2 * jitter + 1)) -
+          jitter;
+    next[best] = t + T + d;
+  }
+  free(next);
+  free(count);
+  return e;
+}
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Toy model: softmax regression (SURVEY config 1; stands in for the worker's forward/backward). fp64. */
+double orc_softmax_loss_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const double *W,
+                             double *grad) {
+  double *z = (double *)malloc((size_t)C * sizeof(double));
+  double loss = 0.0;
+  for (int64_t i = 0; i < (int64_t)d * C; i++) grad[i] = 0.0;
+  for (int32_t b = 0; b < B; b++) {
+    const float *x = X + (int64_t)b * d;
+    for (int32_t c = 0; c < C; c++) {            /* logits z = x W */
+      double acc = 0.0;
+      for (int32_t i = 0; i < d; i++) acc += (double)x[i] * W[(int64_t)i * C + c];
+      z[c] = acc;
+    }
+    double m = z[0];
+    for (int32_t c = 1; c < C; c++) if (z[c] > m) m = z[c];
+    double den = 0.0;
+    for (int32_t c = 0; c < C; c++) den += exp(z[c] - m);
+    loss += -((z[y[b]] - m) - log(den));         /* -log p_{b,y_b} */
+    for (int32_t c = 0; c < C; c++) {
+      double p = exp(z[c] - m) / den;
+      double r = (p - (c == y[b] ? 1.0 : 0.0)) / (double)B;
+      for (int32_t i = 0; i < d; i++) grad[(int64_t)i * C + c] += (double)x[i] * r;   /* X^T (p - Y) / B */
+    }
+  }
+  free(z);
+  return loss / (double)B;
+}
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Straggler detection ("a worker k is identified as a straggler if its training throughput over a sliding
+ * window S_k is lower than the difference between the cluster average and standard deviation S - sigma, for a
+ * number of consecutive detection windows"). sigma is the population standard deviation (reading C14). */
+struct orc_detector {
+  int32_t n, K;
+  int32_t *run;        /* consecutive flagged windows per worker */
+  int32_t clean_run;   /* consecutive windows with no worker flagged */
+};
+
+orc_detector *orc_detector_new(int32_t n, int32_t K) {
+  if (n < 1 || K < 1) return NULL;
+  orc_detector *dt = (orc_detector *)calloc(1, sizeof(orc_detector));
+  dt->n = n; dt->K = K;
+  dt->run = (int32_t *)calloc((size_t)n, sizeof(int32_t));
+  return dt;
+}
+
+void orc_detector_free(orc_detector *dt) {
+  if (!dt) return;
+  free(dt->run);
+  free(dt);
+}
+
+int32_t orc_detector_window(orc_detector *dt, const double *samples, const double *busy, int32_t *straggler) {
+  int32_t n = dt->n;
+  double *Sk = (double *)malloc((size_t)n * sizeof(double));
+  double mean = 0.0;
+  for (int32_t k = 0; k < n; k++) {
+    Sk[k] = busy[k] > 0.0 ? samples[k] / busy[k] : 0.0;
+    mean += Sk[k];
+  }
+  mean /= (double)n;
+  double var = 0.0;
+  for (int32_t k = 0; k < n; k++) var += (Sk[k] - mean) * (Sk[k] - mean);
+  double sigma = sqrt(var / (double)n);
+  int32_t any = 0;
+  for (int32_t k = 0; k < n; k++) {
+    int32_t flagged = Sk[k] < mean - sigma;
+    dt->run[k] = flagged ? dt->run[k] + 1 : 0;
+    straggler[k] = dt->run[k] >= dt->K;
+    any |= flagged;
+  }
+  dt->clean_run = any ? 0 : dt->clean_run + 1;
+  free(Sk);
+  return dt->clean_run >= dt->K;
+}

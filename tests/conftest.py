@@ -1,0 +1,34 @@
+"""Shared pytest configuration.
+
+Markers: ``gpu`` — needs a B200 (the CUDA path, run with ``-m gpu`` on the GPU box). Everything else runs on CPU.
+"""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 device (parity tests through the C-ABI)")
+
+
+def golden(name):
+    """Rows of a tests/golden fixture (comments stripped)."""
+    rows = []
+    with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if line:
+                rows.append(line.split())
+    return rows
+
+
+@pytest.fixture(scope="session")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
