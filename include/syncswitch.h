@@ -1,0 +1,234 @@
+/*
+ * syncswitch.h — C-ABI of the B200-native Sync-Switch synchronization path (arXiv 2104.08364).
+ *
+ * The library (`libsyncswitch.so`, built from paper_2104_08364_b200/csrc/) implements the collocated, sharded
+ * parameter-server synchronization step of Sync-Switch — BSP, ASP and the runtime protocol switch — with
+ * hand-written sm_100a CUDA kernels and NCCL over NVLink. Citation shorthand: P:L = PAPER.md line L, S:L = SPEC.md
+ * line L, SV = SURVEY.md, DESIGN = DESIGN.md at the repo root.
+ *
+ * Conventions (SV §8b):
+ *  - Every call returns an ss_status; none throws or aborts. On error nothing is applied ("errors never partially
+ *    apply"); ss_last_error() describes the most recent error of that context.
+ *  - Integer protocol results (versions, staleness, histogram, dropped count) are computed on the host and are
+ *    final when the call returns. Device data movement is stream-ordered on the context's stream and may be
+ *    batched lazily (ASP windows); it is complete after ss_sync().
+ *  - Pointers documented "host or device" may point to device memory (cudaMalloc / torch CUDA tensors), pinned or
+ *    pageable host memory; host data is staged through device buffers with copies on the context's stream.
+ *  - Buffers passed to a call are BORROWED until the next ss_sync() returns (the library may read/write them
+ *    lazily); params passed to ss_init are COPIED. The caller keeps ownership of every buffer it passes.
+ *  - A context is not thread-safe: one thread per context, calls in program order.
+ *  - SS_E_DIVERGED is sticky: once a non-finite parameter or momentum value is produced (detected on the device,
+ *    surfaced no later than the next ss_sync), every later call returns it ("failed training").
+ *  - Multi-GPU (one process per GPU): after ss_init_dist, ss_bsp_step, ss_asp_push, ss_pull, ss_asp_replay,
+ *    ss_switch, ss_sync and ss_read_params are collective: every rank makes the same call sequence (SPMD).
+ */
+#ifndef SYNCSWITCH_H
+#define SYNCSWITCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ss_ctx ss_ctx;
+
+typedef enum { SS_BSP = 0, SS_ASP = 1 } ss_protocol;
+
+typedef enum {
+  SS_OK = 0,
+  SS_E_INVAL = 1,     /* null pointer, n_params < 1, shards < 1, workers < 1 or > 256, lr <= 0, momentum not in
+                         [0,1), worker id out of range, bad schedule, unsupported layout                           */
+  SS_E_STATE = 2,     /* call invalid in the current protocol (bsp_step under ASP; asp_push under BSP — a late
+                         in-flight push after an ASP->BSP switch lands here and is counted in dropped_pushes,
+                         S:276), a second pending switch, or a multi-GPU call out of order                         */
+  SS_E_PROTOCOL = 3,  /* BSP: missing or duplicate worker in a superstep                                   */
+  SS_E_BARRIER = 4,   /* BSP: a gradient's base version != current version                                 */
+  SS_E_CAUSALITY = 5, /* ASP: base version > current version                                              */
+  SS_E_DIVERGED = 6,  /* non-finite value produced; sticky                                          */
+  SS_E_CUDA = 7,      /* CUDA runtime error (message in ss_last_error)                                             */
+  SS_E_NCCL = 8,      /* NCCL error                                                                               */
+  SS_E_OOM = 9        /* device allocation failed                                                                  */
+} ss_status;
+
+/* ============================================================================================================
+ * Lifecycle
+ * ============================================================================================================ */
+
+/* Create the synchronization state on the current CUDA device (P:1071 collocated PS per worker; P:15 shards).
+ *   params    host or device fp32[n_params], COPIED: the initial model w ("w is a large vector distributed
+ *             into parameter servers").
+ *   n_shards  S >= 1 PS shards: contiguous, equal, padded to 32 floats (128 B); shard s covers
+ *             [min(s*pad, P), min((s+1)*pad, P)) with pad = ceil(ceil(P/S)/32)*32 (SV §8a a1).
+ *   n_workers n in [1, 256] ("equal numbers of PSs and workers" is the paper's default, not required).
+ *   lr        base learning rate eta > 0; momentum mu in [0, 1) ("SGD with momentum of 0.9").
+ * Default policy: protocol BSP at version 0 ("start with BSP"), BSP lr = n*eta, ASP lr = eta/sqrt(n)
+ * (P:1490), no lr decay, weight decay 0. Momentum v = 0. Errors: SS_E_INVAL, SS_E_OOM, SS_E_CUDA (*out = NULL). */
+ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n_shards, int32_t n_workers,
+                  float lr, float momentum);
+
+/* Join `world` ranks (one process per GPU, one context per process) into one sharded PS. Collective; call once
+ * before the first step. nccl_unique_id: the 128-byte ncclUniqueId created by rank 0 and broadcast by the caller.
+ * Shard s is owned by rank floor(s*world/S); worker j is hosted on rank floor(j*world/n) (SV §8a a1).
+ * Requires S % world == 0 (equal owner regions for reduce-scatter / all-gather). Errors: SS_E_INVAL, SS_E_STATE
+ * (already stepped or already distributed), SS_E_NCCL. */
+ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *nccl_unique_id);
+
+/* Fills the 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
+ss_status ss_nccl_unique_id(void *out128);
+
+/* Releases every device buffer, the stream and the communicator. Flushes pending work first. NULL is a no-op. */
+void ss_destroy(ss_ctx *ctx);
+
+/* Human-readable description of the last error on ctx (never NULL; "" when none). */
+const char *ss_last_error(const ss_ctx *ctx);
+
+/* ============================================================================================================
+ * Policy (configuration policy P:1472-1474, schedule P:1600, Table I)
+ * ============================================================================================================ */
+
+/* Piecewise-constant lr decay in the VERSION coordinate (Table I's "total steps"): the factor is 1 before
+ * boundaries[0] and factors[i] from boundaries[i] on (multipliers of the base lr, not cumulative).
+ * boundaries strictly ascending, >= 0; factors > 0; n in [0, 64]. Copied. Errors: SS_E_INVAL. */
+ss_status ss_set_lr_schedule(ss_ctx *ctx, const int64_t *boundaries, const float *factors, int32_t n);
+
+/* asp_rule: 0 -> eta_ASP = eta/sqrt(n), 1 -> eta/n, 2 -> eta. weight_decay lambda >= 0: f(w) = lambda*w
+ * added to each gradient at apply time at the PS's current w ("g11 + f(w0)"). Errors: SS_E_INVAL. */
+ss_status ss_set_lr_policy(ss_ctx *ctx, int32_t asp_rule, float weight_decay);
+
+/* lr used for the next update under `protocol`: (float)((double)eta * factor(version) * scale(protocol)). */
+ss_status ss_current_lr(ss_ctx *ctx, int32_t protocol, float *lr_out);
+
+/* ============================================================================================================
+ * The synchronization path
+ * ============================================================================================================ */
+
+/* BSP superstep (Fig. 3: gradients are aggregated at a barrier, then the model is updated).
+ *   grads[i]    host or device fp32[n_params]: the gradient of worker workers[i] (BORROWED until ss_sync).
+ *   versions[i] the base version that gradient was computed on; must equal the current version.
+ *   n_local     number of gradients supplied. Single GPU: exactly the n workers, each once. Multi-GPU: exactly
+ *               the workers hosted on this rank.
+ * Computes g = (sum_{j ascending} g_j) / n (+ lambda*w), v = mu*v + g, w = w - eta_BSP*v over every shard
+ * (kernel bsp_update; G > 1: local sum -> NCCL reduce-scatter -> owner update -> NCCL all-gather), then
+ * version += 1 and every worker's base version = version; n staleness-0 records.
+ * Errors: SS_E_STATE (protocol is ASP), SS_E_PROTOCOL (missing/duplicate worker), SS_E_BARRIER, SS_E_INVAL. */
+ss_status ss_bsp_step(ss_ctx *ctx, const float *const *grads, const int32_t *workers, const int64_t *versions,
+                      int32_t n_local);
+
+/* ASP push (w1 = w0 - eta_t(g11 + f(w0)) applied on arrival). grad: host or device fp32[n_params] of
+ * `worker`, BORROWED until ss_sync (multi-GPU: non-NULL only on the rank hosting `worker`; NULL elsewhere).
+ * version: the worker's base version (from its last ss_pull). Returns *staleness_out = current - version
+ * immediately, then version += 1. The update itself is applied by the asp_replay kernel when the
+ * window is flushed (window full, ss_pull with a pending window, ss_sync, ss_switch, ss_bsp_step, ss_read_params).
+ * Errors: SS_E_STATE (protocol is BSP; counted in dropped_pushes), SS_E_CAUSALITY, SS_E_INVAL. */
+ss_status ss_asp_push(ss_ctx *ctx, int32_t worker, const float *grad, int64_t version, int64_t *staleness_out);
+
+/* Pull ("a worker will first pull model parameters from all PSs"). dst: host or device fp32[n_params]
+ * (BORROWED until ss_sync; NULL = version only; multi-GPU: non-NULL only on the rank hosting `worker`). Receives
+ * the parameters after exactly the pushes that precede this call, valid after ss_sync. *version_out = current
+ * version; it becomes the worker's base version. Errors: SS_E_INVAL. */
+ss_status ss_pull(ss_ctx *ctx, int32_t worker, float *dst, int64_t *version_out);
+
+/* Switch to `protocol` when the version reaches at_step (at_step <= current: now). w, v and version are carried
+ * over bit-identically (P:280 momentum carried over; P:1531 the prototype's checkpoint/relaunch becomes an in-place
+ * flip). ASP -> BSP drops in-flight pushes and sets every worker's base version to the switch version (every worker
+ * implicitly pulls). One pending switch at a time. Errors: SS_E_INVAL, SS_E_STATE (a switch is already pending). */
+ss_status ss_switch(ss_ctx *ctx, int32_t protocol, int64_t at_step);
+
+/* Batched ASP fast path: identical semantics to the equivalent ss_asp_push / ss_pull call sequence (kind 0 = push
+ * with grad and version; kind 1 = pull into dst, its version is written to staleness_out[i]). Stops at the first
+ * failing event and returns its status; events before it are applied. staleness_out: int64[n_ev] or NULL. */
+typedef struct {
+  int32_t kind;    /* 0 push, 1 pull */
+  int32_t worker;
+  int64_t version; /* push: base version */
+  const float *grad;
+  float *dst;
+} ss_event;
+ss_status ss_asp_replay(ss_ctx *ctx, const ss_event *ev, int64_t n_ev, int64_t *staleness_out);
+
+/* Flush pending windows, wait for the context's stream, surface asynchronous errors (SS_E_DIVERGED, SS_E_CUDA). */
+ss_status ss_sync(ss_ctx *ctx);
+
+/* Copies the unpadded parameters w (fp32[n_params]) / momentum v to a HOST buffer (collective when distributed).
+ * Flushes and synchronizes first. */
+ss_status ss_read_params(ss_ctx *ctx, float *host_dst);
+ss_status ss_read_velocity(ss_ctx *ctx, float *host_dst);
+
+/* Protocol counters: current version, protocol, staleness histogram hist[0..hist_len) (BSP updates count as
+ * staleness 0), pushes dropped at ASP->BSP switches. Any output may be NULL. */
+ss_status ss_get_stats(ss_ctx *ctx, int64_t *version, int32_t *protocol, uint64_t *hist, int32_t hist_len,
+                       uint64_t *dropped_pushes);
+
+/* Applied-gradient log, one record per applied gradient in apply order: {worker, base version, staleness, version
+ * at apply}. Writes min(cap, total) records to rec4 (int64[4*cap]); *total_out = number of records. */
+ss_status ss_get_log(ss_ctx *ctx, int64_t *rec4, int64_t cap, int64_t *total_out);
+
+/* ============================================================================================================
+ * Execution control and instrumentation
+ * ============================================================================================================ */
+
+/* Maximum events (pushes + pulls) per ASP replay window, 1..64 (default 16). Flushes first. */
+ss_status ss_set_window(ss_ctx *ctx, int32_t max_events);
+/* The cudaStream_t all work of this context is ordered on (owned by the context). */
+ss_status ss_get_stream(ss_ctx *ctx, void **stream_out);
+/* Order the context's work after `stream` (cudaStream_t) — used when gradients are produced on another stream. */
+ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
+/* Kernel timing: when on, every bsp_update / asp_replay launch is bracketed by CUDA events on the context's stream;
+ * ss_kernel_stats returns per-kernel launch count, total device milliseconds and algorithmic HBM bytes
+ * (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum). Reading synchronizes. */
+ss_status ss_profile(ss_ctx *ctx, int32_t on);
+ss_status ss_kernel_stats(ss_ctx *ctx, int32_t kernel_id, int64_t *launches, double *total_ms, double *bytes);
+
+/* ============================================================================================================
+ * Seeded synthetic inputs and the toy model (SV §8d; kernels synth_grad and softmax_grad)
+ * ============================================================================================================ */
+
+/* dst[t] = g(seed, j, k, i0 + t) for t in [0, count): key = (j<<56) ^ (k<<30) ^ i, h = splitmix64(seed ^ key),
+ * g = ((h>>40)*2^-24 - 0.5)*2^-6 (exact in fp32, uniform in [-1/128, 1/128)). dst: device fp32[count];
+ * stream: cudaStream_t or NULL (legacy default stream). j < 256, k < 2^26, i0 + count <= 2^30. */
+ss_status ss_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst, void *stream);
+
+/* Softmax regression (stands in for the worker's forward/backward): X device fp32[B*d] row-major,
+ * y device int32[B], W device fp32[d*C] row-major (P = d*C). grad = X^T (softmax(XW) - onehot(y)) / B into device
+ * fp32[d*C]; *loss_dev (device fp32[1]) = mean cross-entropy. B <= 1024, C <= 32. */
+ss_status ss_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                          float *grad, float *loss_dev, void *stream);
+
+/* ============================================================================================================
+ * Control plane (host only; no GPU needed)
+ * ============================================================================================================ */
+
+/* Table I workload-preserving remap: BSP steps = W*s/(B*N), ASP steps = W/B - W*s/B with s = s_num/s_den;
+ * boundary W_i (samples) -> W_i/(B*N) if W_i <= W*s, else W_i/B - W*s/B + W*s/(B*N) (DESIGN reading C11).
+ * Errors: SS_E_INVAL when a quantity is not integral. */
+ss_status ss_table1(int64_t W, int64_t B, int64_t N, int64_t s_num, int64_t s_den, const int64_t *Wb, int32_t nb,
+                    int64_t *bsp_steps, int64_t *asp_steps, int64_t *bounds_out);
+
+/* Seeded integer-tick arrival schedule (DESIGN reading C7): all n workers pull at t = 0; worker j's k-th push at
+ * t_{j,k} = t_{j,k-1} + T_j(t_{j,k-1}) + d_{j,k}, immediately followed by its pull; global order by (t, j).
+ * T_j(t) = period[j] * slow_factor when j == slow_worker and slow_t0 <= t < slow_t1; d_{j,k} =
+ * (splitmix64(seed ^ (j<<32) ^ k) mod (2J+1)) - J. Writes n + 2*n_push events to kind/worker/tick (capacity
+ * n + 2*n_push each); *n_out = events written. Errors: SS_E_INVAL (period <= J, n out of range). */
+ss_status ss_schedule(int32_t n, const int64_t *period, int64_t jitter, uint64_t seed, int32_t slow_worker,
+                      int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t n_push, int32_t *kind,
+                      int32_t *worker, int64_t *tick, int64_t *n_out);
+
+/* Straggler detector: per window, S_k = samples[k]/busy[k]; worker k is flagged when S_k < mean - sigma
+ * (population sigma) and is a straggler after K consecutive flagged windows; *clean_out = 1 when no worker was
+ * flagged for the last K windows ("cluster free of stragglers"). */
+typedef struct ss_detector ss_detector;
+ss_status ss_detector_new(ss_detector **out, int32_t n, int32_t K);
+ss_status ss_detector_window(ss_detector *dt, const double *samples, const double *busy, int32_t *straggler,
+                             int32_t *clean_out);
+void ss_detector_free(ss_detector *dt);
+
+/* Greedy online policy: given the detector's verdict, the protocol and the BSP quota, returns the switch
+ * to issue now: -1 none, SS_ASP (a straggler appeared during BSP), SS_BSP (cluster clean, ASP, BSP quota unmet). */
+int32_t ss_greedy_decision(int32_t protocol, int32_t any_straggler, int32_t cluster_clean, int64_t bsp_done,
+                           int64_t bsp_quota);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYNCSWITCH_H */

@@ -1,0 +1,63 @@
+// internal.h — launch interfaces shared by runtime.cu and kernels.cu (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ss {
+
+constexpr int kMaxWorkers = 256;  // SV §8b: workers in [1, 256]
+constexpr int kMaxEvents = 64;    // events per ASP replay window
+
+// bsp_update (SV §2.5 K1): out-of-place aggregate of n_in inputs in ascending order, mean by `divisor`,
+// momentum update of the owner slice. 1-GPU form: inputs = the n worker gradients, divisor = n. Post-reduce-scatter
+// form: inputs = {reduce-scattered sum}, divisor = n. All pointers are pre-offset to the slice; `count` elements.
+struct BspArgs {
+  const float *g[kMaxWorkers];
+  float *w;
+  float *v;
+  int *flag;          // set to 1 when a non-finite w or v is produced
+  int64_t count;
+  int32_t n_in;
+  float divisor;
+  float mu;
+  float neg_eta;
+  float lam;
+};
+
+// local_sum: out[i] = sum_{j ascending} g[j][i] for i < count, 0 for count <= i < count_pad (multi-GPU pre-sum
+// of the workers hosted on one rank before the reduce-scatter).
+struct SumArgs {
+  const float *g[kMaxWorkers];
+  float *out;
+  int64_t count;
+  int64_t count_pad;
+  int32_t n_in;
+};
+
+// asp_replay (SV §2.5 K2): a window of pushes and pulls applied in arrival order to one owner slice.
+struct AspEvent {
+  const float *src;   // push: gradient slice
+  float *dst;         // pull: snapshot destination slice (nullptr: no data)
+  float lr;           // push: eta_ASP at the push's version
+  int32_t kind;       // 0 push, 1 pull
+};
+struct AspArgs {
+  AspEvent ev[kMaxEvents];
+  float *w;
+  float *v;
+  int *flag;
+  int64_t count;
+  int32_t n_ev;
+  float mu;
+  float lam;
+};
+
+cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s);
+cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s);
+cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s);
+cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
+                              cudaStream_t s);
+cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                                float *grad, float *loss, float *scratch, cudaStream_t s);
+
+}  // namespace ss

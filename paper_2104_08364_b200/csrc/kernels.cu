@@ -1,0 +1,465 @@
+// kernels.cu — sm_100a kernels of the Sync-Switch synchronization path.
+//
+//   bsp_update   (K1) fused aggregate + mean + momentum update of an owner slice
+//   local_sum    (K1a) ascending pre-sum of the workers hosted on one rank (G > 1)
+//   asp_replay   (K2) a window of ASP pushes/pulls applied in arrival order
+//   synth_grad   (K3) seeded counter-hash gradients                      —
+//   softmax_grad (K4) toy softmax-regression loss and gradient (SURVEY config 1)     P:1072 (worker fwd/bwd)
+//
+// The path is HBM-bound streaming (arithmetic intensity ~0.25 flop/B, no contraction): no tensor cores. Every
+// kernel moves 128-bit vectors with streaming cache hints, keeps many independent loads in flight per thread
+// (all inputs of a chunk are issued before the dependent arithmetic), and runs a grid sized to the SM count.
+// Floating-point order is fixed and explicit (__fadd_rn / __fmaf_rn / __fdiv_rn) so that results are bit-identical
+// to the CPU oracle's written order (reading C12): sum in ascending worker order, then the mean, then
+// v = fma(mu, v, g), w = fma(-eta, v, w).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace ss {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float4 ld4(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ void st4(float *p, float4 x) { __stcs(reinterpret_cast<float4 *>(p), x); }
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ bool nonfinite(float x) { return !isfinite(x); }
+
+// g = a / divisor (+ lam*w); v = mu*v + g; w = w - eta*v.  When the divisor is a power of two, a*recip is the same
+// correctly rounded quotient, so `use_recip` changes no bit.
+struct Upd {
+  float divisor, recip, mu, neg_eta, lam;
+  bool use_recip;
+  __device__ __forceinline__ void operator()(float a, float &w, float &v) const {
+    float g = use_recip ? __fmul_rn(a, recip) : __fdiv_rn(a, divisor);
+    if (lam != 0.0f) g = __fmaf_rn(lam, w, g);
+    v = __fmaf_rn(mu, v, g);
+    w = __fmaf_rn(neg_eta, v, w);
+  }
+};
+
+__device__ __forceinline__ bool is_pow2(float d) {
+  int e;
+  return frexpf(d, &e) == 0.5f;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// K1 bsp_update
+constexpr int kU1 = 2;  // float4 chunks per thread per iteration
+constexpr int kG1 = 8;  // gradients loaded together
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
+  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  if (VEC) {
+    const int64_t n4 = a.count >> 2;
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * kU1) {
+      float4 acc[kU1], wv[kU1], vv[kU1];
+      bool ok[kU1];
+#pragma unroll
+      for (int u = 0; u < kU1; ++u) {
+        const int64_t q = q0 + u * stride;
+        ok[u] = q < n4;
+        if (ok[u]) {
+          acc[u] = ld4(a.g[0] + 4 * q);
+          wv[u] = ld4(a.w + 4 * q);
+          vv[u] = ld4(a.v + 4 * q);
+        }
+      }
+      for (int j0 = 1; j0 < a.n_in; j0 += kG1) {
+        float4 t[kG1][kU1];
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < kU1; ++u)
+            if (j0 + jj < a.n_in && ok[u]) t[jj][u] = ld4(a.g[j0 + jj] + 4 * (q0 + u * stride));
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < kU1; ++u)
+            if (j0 + jj < a.n_in && ok[u]) acc[u] = add4(acc[u], t[jj][u]);  // ascending worker order
+      }
+#pragma unroll
+      for (int u = 0; u < kU1; ++u) {
+        if (!ok[u]) continue;
+        up(acc[u].x, wv[u].x, vv[u].x);
+        up(acc[u].y, wv[u].y, vv[u].y);
+        up(acc[u].z, wv[u].z, vv[u].z);
+        up(acc[u].w, wv[u].w, vv[u].w);
+        bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
+               nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
+        const int64_t q = q0 + u * stride;
+        st4(a.w + 4 * q, wv[u]);
+        st4(a.v + 4 * q, vv[u]);
+      }
+    }
+    // scalar tail (count % 4 elements)
+    const int64_t i = 4 * n4 + tid;
+    if (i < a.count) {
+      float acc = a.g[0][i];
+      for (int j = 1; j < a.n_in; ++j) acc = __fadd_rn(acc, a.g[j][i]);
+      float w = a.w[i], v = a.v[i];
+      up(acc, w, v);
+      bad |= nonfinite(w) | nonfinite(v);
+      a.w[i] = w;
+      a.v[i] = v;
+    }
+  } else {
+    for (int64_t i = tid; i < a.count; i += stride) {
+      float acc = a.g[0][i];
+      for (int j = 1; j < a.n_in; ++j) acc = __fadd_rn(acc, a.g[j][i]);
+      float w = a.w[i], v = a.v[i];
+      up(acc, w, v);
+      bad |= nonfinite(w) | nonfinite(v);
+      a.w[i] = w;
+      a.v[i] = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// K1a local_sum
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) local_sum_kernel(const __grid_constant__ SumArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (VEC) {
+    const int64_t n4 = a.count >> 2;
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * kU1) {
+      float4 acc[kU1];
+      bool ok[kU1];
+#pragma unroll
+      for (int u = 0; u < kU1; ++u) {
+        const int64_t q = q0 + u * stride;
+        ok[u] = q < n4;
+        if (ok[u]) acc[u] = ld4(a.g[0] + 4 * q);
+      }
+      for (int j0 = 1; j0 < a.n_in; j0 += kG1) {
+        float4 t[kG1][kU1];
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < kU1; ++u)
+            if (j0 + jj < a.n_in && ok[u]) t[jj][u] = ld4(a.g[j0 + jj] + 4 * (q0 + u * stride));
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < kU1; ++u)
+            if (j0 + jj < a.n_in && ok[u]) acc[u] = add4(acc[u], t[jj][u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kU1; ++u)
+        if (ok[u]) st4(a.out + 4 * (q0 + u * stride), acc[u]);
+    }
+    done = 4 * n4;
+  }
+  for (int64_t i = done + tid; i < a.count_pad; i += stride) {
+    float acc = 0.0f;
+    if (i < a.count) {
+      acc = a.g[0][i];
+      for (int j = 1; j < a.n_in; ++j) acc = __fadd_rn(acc, a.g[j][i]);
+    }
+    a.out[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// K2 asp_replay. Each thread owns kU2 float4 chunks of the slice for the whole window: w and v are read once and
+// written once per window; every push streams its gradient chunk in (prefetched one push ahead), every pull
+// stores the current w chunk — so a pull observes exactly the pushes before it, on every shard (reading C6).
+constexpr int kU2 = 4;
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_constant__ AspArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float mu = a.mu, lam = a.lam;
+  bool bad = false;
+  int first_push = 0;
+  while (first_push < a.n_ev && a.ev[first_push].kind != 0) ++first_push;
+
+  auto apply1 = [&](float g, float &w, float &v, float neg_eta) {
+    if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
+    v = __fmaf_rn(mu, v, g);
+    w = __fmaf_rn(neg_eta, v, w);
+  };
+
+  if (VEC) {
+    const int64_t n4 = a.count >> 2;
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * kU2) {
+      float4 wv[kU2], vv[kU2], gn[kU2];
+      bool ok[kU2];
+#pragma unroll
+      for (int u = 0; u < kU2; ++u) {
+        const int64_t q = q0 + u * stride;
+        ok[u] = q < n4;
+        if (ok[u]) {
+          wv[u] = ld4(a.w + 4 * q);
+          vv[u] = ld4(a.v + 4 * q);
+          if (first_push < a.n_ev) gn[u] = ld4(a.ev[first_push].src + 4 * q);
+        }
+      }
+      int next = first_push;
+      for (int e = 0; e < a.n_ev; ++e) {
+        const int kind = a.ev[e].kind;
+        if (kind == 0) {
+          float4 gc[kU2];
+#pragma unroll
+          for (int u = 0; u < kU2; ++u) gc[u] = gn[u];
+          next = e + 1;
+          while (next < a.n_ev && a.ev[next].kind != 0) ++next;
+          if (next < a.n_ev) {
+#pragma unroll
+            for (int u = 0; u < kU2; ++u)
+              if (ok[u]) gn[u] = ld4(a.ev[next].src + 4 * (q0 + u * stride));
+          }
+          const float neg_eta = -a.ev[e].lr;
+#pragma unroll
+          for (int u = 0; u < kU2; ++u) {
+            if (!ok[u]) continue;
+            apply1(gc[u].x, wv[u].x, vv[u].x, neg_eta);
+            apply1(gc[u].y, wv[u].y, vv[u].y, neg_eta);
+            apply1(gc[u].z, wv[u].z, vv[u].z, neg_eta);
+            apply1(gc[u].w, wv[u].w, vv[u].w, neg_eta);
+          }
+        } else if (a.ev[e].dst != nullptr) {
+          float *dst = a.ev[e].dst;
+#pragma unroll
+          for (int u = 0; u < kU2; ++u)
+            if (ok[u]) st4(dst + 4 * (q0 + u * stride), wv[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU2; ++u) {
+        if (!ok[u]) continue;
+        bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
+               nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
+        const int64_t q = q0 + u * stride;
+        st4(a.w + 4 * q, wv[u]);
+        st4(a.v + 4 * q, vv[u]);
+      }
+    }
+    const int64_t i = 4 * n4 + tid;
+    if (i < a.count) {
+      float w = a.w[i], v = a.v[i];
+      for (int e = 0; e < a.n_ev; ++e) {
+        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr);
+        else if (a.ev[e].dst) a.ev[e].dst[i] = w;
+      }
+      bad |= nonfinite(w) | nonfinite(v);
+      a.w[i] = w;
+      a.v[i] = v;
+    }
+  } else {
+    for (int64_t i = tid; i < a.count; i += stride) {
+      float w = a.w[i], v = a.v[i];
+      for (int e = 0; e < a.n_ev; ++e) {
+        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr);
+        else if (a.ev[e].dst) a.ev[e].dst[i] = w;
+      }
+      bad |= nonfinite(w) | nonfinite(v);
+      a.w[i] = w;
+      a.v[i] = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// K3 synth_grad: g = ((h >> 40) * 2^-24 - 0.5) * 2^-6 with h = splitmix64(seed ^ ((j<<56) ^ (k<<30) ^ i)).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float synth1(uint64_t seed, uint64_t jk, uint64_t i) {
+  const uint64_t h = splitmix64(seed ^ (jk ^ i));
+  const float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);  // * 2^-24, exact
+  return __fmul_rn(__fadd_rn(u, -0.5f), 0.015625f);                                // exact
+}
+
+__global__ void __launch_bounds__(kThreads) synth_grad_kernel(uint64_t seed, uint64_t jk, int64_t i0, int64_t count,
+                                                              float *dst, bool vec) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n4 = count >> 2;
+    for (int64_t q = tid; q < n4; q += stride) {
+      const uint64_t i = (uint64_t)(i0 + 4 * q);
+      st4(dst + 4 * q, make_float4(synth1(seed, jk, i), synth1(seed, jk, i + 1), synth1(seed, jk, i + 2),
+                                   synth1(seed, jk, i + 3)));
+    }
+    done = 4 * n4;
+  }
+  for (int64_t t = done + tid; t < count; t += stride) dst[t] = synth1(seed, jk, (uint64_t)(i0 + t));
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// K4 softmax regression: logits z = x W (W is d x C row-major), p = softmax(z), r = (p - onehot(y)) / B,
+// grad = X^T r, loss = mean_b(-log p_{b,y_b}). Two small kernels; fixed summation orders (deterministic).
+constexpr int kMaxC = 32;
+
+__global__ void __launch_bounds__(kThreads) softmax_fwd_kernel(const float *X, const int32_t *y, int32_t B,
+                                                               int32_t d, int32_t C, const float *W, float *r,
+                                                               float *loss_b) {
+  const int b = blockIdx.x;
+  const float *x = X + (int64_t)b * d;
+  float part[kMaxC];
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) part[c] = 0.0f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float xi = x[i];
+    const float *wr = W + (int64_t)i * C;
+#pragma unroll
+    for (int c = 0; c < kMaxC; ++c)
+      if (c < C) part[c] = __fmaf_rn(xi, wr[c], part[c]);
+  }
+  __shared__ float red[kThreads / 32][kMaxC];
+  __shared__ float z[kMaxC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < kMaxC; ++c) {
+    if (c >= C) break;
+    float s = part[c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) red[wid][c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < C) {
+    float s = 0.0f;
+    for (int k = 0; k < kThreads / 32; ++k) s += red[k][threadIdx.x];
+    z[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = z[0];
+    for (int c = 1; c < C; ++c) m = fmaxf(m, z[c]);
+    float den = 0.0f;
+    for (int c = 0; c < C; ++c) den += expf(z[c] - m);
+    const int yb = y[b];
+    loss_b[b] = -((z[yb] - m) - logf(den));
+    for (int c = 0; c < C; ++c) {
+      const float p = expf(z[c] - m) / den;
+      r[(int64_t)b * C + c] = (p - (c == yb ? 1.0f : 0.0f)) / (float)B;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float *X, int32_t B, int32_t d, int32_t C,
+                                                               const float *r, const float *loss_b, float *grad,
+                                                               float *loss) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < (int64_t)d * C) {
+    const int64_t i = idx / C;
+    const int c = (int)(idx % C);
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s = __fmaf_rn(X[(int64_t)b * d + i], r[(int64_t)b * C + c], s);
+    grad[idx] = s;
+  }
+  if (idx == 0) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += loss_b[b];
+    *loss = s / (float)B;
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Grid: enough CTAs for the work, capped at (resident CTAs per SM) x (SM count) — one full wave of a persistent
+// grid-stride kernel (B200: 148 SMs).
+template <typename K>
+int grid_for(K kernel, int64_t work_items) {
+  static thread_local int resident = 0;
+  int r = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
+  resident = r > 0 ? r : 1;
+  int64_t want = (work_items + kThreads - 1) / kThreads;
+  int64_t cap = (int64_t)resident * num_sms();
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+}  // namespace
+
+cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
+  if (a.count <= 0) return cudaSuccess;
+  if (vec) {
+    auto k = bsp_update_kernel<true>;
+    k<<<grid_for(k, (a.count / 4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
+  } else {
+    auto k = bsp_update_kernel<false>;
+    k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
+  if (a.count_pad <= 0) return cudaSuccess;
+  if (vec) {
+    auto k = local_sum_kernel<true>;
+    k<<<grid_for(k, (a.count / 4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
+  } else {
+    auto k = local_sum_kernel<false>;
+    k<<<grid_for(k, a.count_pad), kThreads, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
+  if (a.count <= 0 || a.n_ev <= 0) return cudaSuccess;
+  if (vec) {
+    auto k = asp_replay_kernel<true>;
+    k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);
+  } else {
+    auto k = asp_replay_kernel<false>;
+    k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
+                              cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const uint64_t jk = ((uint64_t)(uint32_t)j << 56) ^ ((uint64_t)k << 30);
+  const bool vec = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  int64_t items = vec ? count / 4 + 1 : count;
+  int64_t want = (items + kThreads - 1) / kThreads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  synth_grad_kernel<<<(int)(want < cap ? want : cap), kThreads, 0, s>>>(seed, jk, i0, count, dst, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                                float *grad, float *loss, float *scratch, cudaStream_t s) {
+  float *r = scratch;
+  float *loss_b = scratch + (int64_t)B * C;
+  softmax_fwd_kernel<<<B, kThreads, 0, s>>>(X, y, B, d, C, W, r, loss_b);
+  const int64_t n = (int64_t)d * C;
+  softmax_bwd_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(X, B, d, C, r, loss_b, grad, loss);
+  return cudaGetLastError();
+}
+
+}  // namespace ss

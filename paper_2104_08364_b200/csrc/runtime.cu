@@ -1,0 +1,790 @@
+// runtime.cu — C-ABI runtime of the Sync-Switch synchronization path (include/syncswitch.h).
+//
+// Host side: shard map (SV §8a a1), version / staleness table and BSP barrier checks (a3, a7), ASP window batcher
+// (a9-a10), switch controller (a11) and lr policy (a12). Device side: w replica [P_pad], momentum v of the owned
+// region, a non-finite flag, gradient / snapshot staging. Multi-GPU: NCCL reduce-scatter -> bsp_update ->
+// all-gather for BSP; grouped send/recv owner routing for ASP windows (SV §8e).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "syncswitch.h"
+
+namespace {
+
+constexpr int kMaxSchedule = 64;
+
+struct Ev {
+  int32_t kind;         // 0 push, 1 pull
+  int32_t worker;
+  const float *src;     // push: device gradient (full length; staged if the caller's was host memory);
+                        //       nullptr on ranks not hosting the worker
+  float *dst;           // pull: device destination (full length) on the hosting rank, else nullptr
+  float *host_dst;      // pull into host memory: D2H from dst after the window
+  float lr;             // push: eta_ASP at the push's (pre-increment) version
+  bool data;            // pull: moves parameters (false: version-only pull, G = 1)
+};
+
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0.0, bytes = 0.0;
+};
+
+struct Timed {
+  cudaEvent_t a, b;
+  int kernel;
+  double bytes;
+};
+
+}  // namespace
+
+struct ss_ctx {
+  // configuration
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t P = 0, pad = 0, P_pad = 0;
+  int32_t S = 0, n = 0;
+  std::vector<int64_t> off;
+  float eta = 0.f, mu = 0.f, lam = 0.f;
+  int32_t asp_rule = 0;
+  std::vector<int64_t> bounds;
+  std::vector<float> factors;
+  // distribution
+  int32_t rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int64_t reg_len = 0;                 // padded owner region length (P_pad / world)
+  std::vector<int64_t> real_lo, real_hi;  // per rank: real (unpadded) element range of its region
+  // device state
+  float *w = nullptr;                  // replica [P_pad]; authoritative on the owned region
+  float *v = nullptr;                  // momentum of the owned region [reg_len]
+  int *flag = nullptr;                 // non-finite flag
+  float *sum_buf = nullptr;            // G > 1: local pre-sum [P_pad]
+  float *rs_buf = nullptr;             // G > 1: reduce-scattered sum [reg_len]
+  std::vector<float *> stage;          // full-length staging slots for host pointers
+  int32_t stage_used = 0;
+  std::vector<float *> rslot, sslot;   // G > 1: received gradient shards / snapshot shards per window event
+  // protocol state (host; bit-exact with the oracle)
+  int64_t version = 0;
+  std::vector<int64_t> base;
+  int32_t proto = SS_BSP;
+  bool has_pending = false;
+  int32_t pending_proto = SS_BSP;
+  int64_t pending_at = 0;
+  std::vector<uint64_t> hist;
+  uint64_t dropped = 0;
+  bool diverged = false;
+  bool stepped = false;
+  std::vector<int64_t> log;            // 4 per applied gradient
+  // window batcher
+  std::vector<Ev> win;
+  int32_t max_win = 16;
+  // instrumentation
+  bool prof = false;
+  std::vector<Timed> timed;
+  KStat kstat[3];
+  std::string err;
+};
+
+namespace {
+
+ss_status fail(ss_ctx *c, ss_status s, const char *fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define SS_CUDA(c, call)                                                                                 \
+  do {                                                                                                   \
+    cudaError_t e_ = (call);                                                                             \
+    if (e_ != cudaSuccess)                                                                               \
+      return fail((c), e_ == cudaErrorMemoryAllocation ? SS_E_OOM : SS_E_CUDA, "%s: %s (%s:%d)", #call, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                           \
+  } while (0)
+
+#define SS_NCCL(c, call)                                                                                        \
+  do {                                                                                                          \
+    ncclResult_t r_ = (call);                                                                                   \
+    if (r_ != ncclSuccess)                                                                                      \
+      return fail((c), SS_E_NCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__);         \
+  } while (0)
+
+#define SS_TRY(expr)              \
+  do {                            \
+    ss_status s_ = (expr);        \
+    if (s_ != SS_OK) return s_;   \
+  } while (0)
+
+bool is_host_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int32_t host_of(const ss_ctx *c, int32_t j) { return (int32_t)(((int64_t)j * c->world) / c->n); }
+
+// lr(version, protocol) = (float)((double)eta * factor(version) * scale(protocol)) — P:1600.
+float lr_at(const ss_ctx *c, int64_t ver, int32_t proto) {
+  double f = 1.0;
+  for (size_t i = 0; i < c->bounds.size(); ++i)
+    if (c->bounds[i] <= ver) f = (double)c->factors[i];
+  double scale;
+  if (proto == SS_BSP) scale = (double)c->n;
+  else if (c->asp_rule == 0) scale = 1.0 / std::sqrt((double)c->n);
+  else if (c->asp_rule == 1) scale = 1.0 / (double)c->n;
+  else scale = 1.0;
+  return (float)((double)c->eta * f * scale);
+}
+
+void record(ss_ctx *c, int64_t worker, int64_t b, int64_t st) {
+  if ((size_t)st >= c->hist.size()) c->hist.resize((size_t)st + 1, 0);
+  c->hist[st] += 1;
+  c->log.push_back(worker);
+  c->log.push_back(b);
+  c->log.push_back(st);
+  c->log.push_back(c->version);
+}
+
+ss_status stage_slot(ss_ctx *c, float **out) {
+  if (c->stage_used == (int32_t)c->stage.size()) {
+    float *p = nullptr;
+    SS_CUDA(c, cudaMalloc(&p, (size_t)c->P_pad * sizeof(float)));
+    c->stage.push_back(p);
+  }
+  *out = c->stage[c->stage_used++];
+  return SS_OK;
+}
+
+// Host gradient -> device staging slot (stream-ordered; the caller's buffer is borrowed until ss_sync).
+ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
+  if (!is_host_ptr(g)) {
+    *out = g;
+    return SS_OK;
+  }
+  float *slot = nullptr;
+  SS_TRY(stage_slot(c, &slot));
+  SS_CUDA(c, cudaMemcpyAsync(slot, g, (size_t)c->P * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  *out = slot;
+  return SS_OK;
+}
+
+void timed_begin(ss_ctx *c, Timed *t, int kernel, double bytes) {
+  if (!c->prof) return;
+  t->kernel = kernel;
+  t->bytes = bytes;
+  cudaEventCreate(&t->a);
+  cudaEventCreate(&t->b);
+  cudaEventRecord(t->a, c->stream);
+}
+
+void timed_end(ss_ctx *c, Timed *t) {
+  if (!c->prof) return;
+  cudaEventRecord(t->b, c->stream);
+  c->timed.push_back(*t);
+}
+
+ss_status drain_timed(ss_ctx *c) {
+  if (c->timed.empty()) return SS_OK;
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (auto &t : c->timed) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    c->kstat[t.kernel].launches += 1;
+    c->kstat[t.kernel].ms += ms;
+    c->kstat[t.kernel].bytes += t.bytes;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  c->timed.clear();
+  return SS_OK;
+}
+
+ss_status ensure_dist_buffers(ss_ctx *c) {
+  if (c->world == 1) return SS_OK;
+  if (!c->sum_buf) SS_CUDA(c, cudaMalloc(&c->sum_buf, (size_t)c->P_pad * sizeof(float)));
+  if (!c->rs_buf) SS_CUDA(c, cudaMalloc(&c->rs_buf, (size_t)c->reg_len * sizeof(float)));
+  while ((int32_t)c->rslot.size() < c->max_win) {
+    float *a = nullptr, *b = nullptr;
+    SS_CUDA(c, cudaMalloc(&a, (size_t)c->reg_len * sizeof(float)));
+    SS_CUDA(c, cudaMalloc(&b, (size_t)c->reg_len * sizeof(float)));
+    c->rslot.push_back(a);
+    c->sslot.push_back(b);
+  }
+  return SS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// ASP window flush: [G>1: grouped send/recv of gradient shards to owners] -> asp_replay on the owned slice ->
+// [G>1: grouped send/recv of snapshot shards to pullers] -> D2H of host destinations.
+ss_status flush(ss_ctx *c) {
+  if (c->win.empty()) {
+    c->stage_used = 0;
+    return SS_OK;
+  }
+  const int32_t me = c->rank;
+  const int64_t lo = c->real_lo[me], hi = c->real_hi[me], cnt = hi - lo;
+  int32_t n_push = 0, n_pull = 0;
+  for (const Ev &e : c->win) {
+    if (e.kind == 0) ++n_push;
+    else if (e.data) ++n_pull;
+  }
+
+  if (c->world > 1) {
+    SS_TRY(ensure_dist_buffers(c));
+    SS_NCCL(c, ncclGroupStart());
+    for (size_t k = 0; k < c->win.size(); ++k) {
+      const Ev &e = c->win[k];
+      if (e.kind != 0) continue;
+      const int32_t h = host_of(c, e.worker);
+      if (h == me) {
+        for (int32_t r = 0; r < c->world; ++r) {
+          const int64_t rc = c->real_hi[r] - c->real_lo[r];
+          if (r != me && rc > 0) SS_NCCL(c, ncclSend(e.src + c->real_lo[r], rc, ncclFloat, r, c->comm, c->stream));
+        }
+      } else if (cnt > 0) {
+        SS_NCCL(c, ncclRecv(c->rslot[k], cnt, ncclFloat, h, c->comm, c->stream));
+      }
+    }
+    SS_NCCL(c, ncclGroupEnd());
+  }
+
+  if (cnt > 0) {
+    if (n_push == 0 && c->world == 1) {
+      // pulls only: plain copies of the current w
+      for (const Ev &e : c->win)
+        if (e.data) SS_CUDA(c, cudaMemcpyAsync(e.dst, c->w, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice,
+                                              c->stream));
+    } else {
+      ss::AspArgs a;
+      std::memset(&a, 0, sizeof a);
+      bool vec = true;
+      int32_t ne = 0;
+      for (size_t k = 0; k < c->win.size(); ++k) {
+        const Ev &e = c->win[k];
+        ss::AspEvent &x = a.ev[ne];
+        x.kind = e.kind;
+        if (e.kind == 0) {
+          x.src = (c->world == 1 || host_of(c, e.worker) == me) ? e.src + lo : c->rslot[k];
+          x.lr = e.lr;
+          vec = vec && aligned16(x.src);
+        } else {
+          if (!e.data) continue;  // version-only pull: no data
+          x.dst = (c->world == 1 || host_of(c, e.worker) == me) ? e.dst + lo : c->sslot[k];
+          vec = vec && aligned16(x.dst);
+        }
+        ++ne;
+      }
+      a.n_ev = ne;
+      a.w = c->w + lo;
+      a.v = c->v;
+      a.flag = c->flag;
+      a.count = cnt;
+      a.mu = c->mu;
+      a.lam = c->lam;
+      Timed t;
+      timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
+      SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
+      timed_end(c, &t);
+    }
+  }
+
+  if (c->world > 1) {
+    SS_NCCL(c, ncclGroupStart());
+    for (size_t k = 0; k < c->win.size(); ++k) {
+      const Ev &e = c->win[k];
+      if (e.kind != 1 || !e.data) continue;
+      const int32_t h = host_of(c, e.worker);
+      if (h == me) {
+        for (int32_t r = 0; r < c->world; ++r) {
+          const int64_t rc = c->real_hi[r] - c->real_lo[r];
+          if (r != me && rc > 0) SS_NCCL(c, ncclRecv(e.dst + c->real_lo[r], rc, ncclFloat, r, c->comm, c->stream));
+        }
+      } else if (cnt > 0) {
+        SS_NCCL(c, ncclSend(c->sslot[k], cnt, ncclFloat, h, c->comm, c->stream));
+      }
+    }
+    SS_NCCL(c, ncclGroupEnd());
+  }
+
+  for (const Ev &e : c->win)
+    if (e.kind == 1 && e.host_dst)
+      SS_CUDA(c, cudaMemcpyAsync(e.host_dst, e.dst, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  c->win.clear();
+  c->stage_used = 0;
+  return SS_OK;
+}
+
+// A pending switch takes effect once version >= at (SV §8c maybe_switch). ASP->BSP: pending window flushed, later
+// pushes of the old phase are rejected and counted (reading C8), every worker's base version becomes V.
+ss_status maybe_switch(ss_ctx *c) {
+  if (c->has_pending && c->version >= c->pending_at) {
+    c->has_pending = false;
+    if (c->pending_proto != c->proto) {
+      SS_TRY(flush(c));
+      c->proto = c->pending_proto;
+      if (c->proto == SS_BSP)
+        for (auto &b : c->base) b = c->version;
+    }
+  }
+  return SS_OK;
+}
+
+ss_status check_live(ss_ctx *c) {
+  if (!c) return SS_E_INVAL;
+  if (c->diverged) return fail(c, SS_E_DIVERGED, "diverged: a non-finite parameter or momentum was produced");
+  return SS_OK;
+}
+
+ss_status enqueue(ss_ctx *c, const Ev &e) {
+  c->win.push_back(e);
+  if ((int32_t)c->win.size() >= c->max_win) return flush(c);
+  return SS_OK;
+}
+
+ss_status sync_impl(ss_ctx *c) {
+  SS_TRY(flush(c));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  int h = 0;
+  SS_CUDA(c, cudaMemcpy(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) c->diverged = true;
+  if (c->diverged) return fail(c, SS_E_DIVERGED, "diverged: a non-finite parameter or momentum was produced");
+  return SS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n_shards, int32_t n_workers,
+                  float lr, float momentum) {
+  if (!out) return SS_E_INVAL;
+  *out = nullptr;
+  if (!params || n_params < 1 || n_shards < 1 || n_workers < 1 || n_workers > ss::kMaxWorkers || !(lr > 0.0f) ||
+      !(momentum >= 0.0f && momentum < 1.0f))
+    return SS_E_INVAL;
+  ss_ctx *c = new (std::nothrow) ss_ctx;
+  if (!c) return SS_E_OOM;
+  c->P = n_params;
+  c->S = n_shards;
+  c->n = n_workers;
+  c->eta = lr;
+  c->mu = momentum;
+  const int64_t per = (n_params + n_shards - 1) / n_shards;
+  c->pad = ((per + 31) / 32) * 32;
+  c->P_pad = c->pad * n_shards;
+  c->off.resize(n_shards + 1);
+  for (int32_t s = 0; s <= n_shards; ++s) c->off[s] = std::min<int64_t>((int64_t)s * c->pad, n_params);
+  c->base.assign(n_workers, 0);
+  c->reg_len = c->P_pad;
+  c->real_lo = {0};
+  c->real_hi = {n_params};
+  auto bail = [&](ss_status s) {
+    ss_destroy(c);
+    return s;
+  };
+  if (cudaGetDevice(&c->device) != cudaSuccess) return bail(SS_E_CUDA);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SS_E_CUDA);
+  if (cudaMalloc(&c->w, (size_t)c->P_pad * sizeof(float)) != cudaSuccess) return bail(SS_E_OOM);
+  if (cudaMalloc(&c->v, (size_t)c->P_pad * sizeof(float)) != cudaSuccess) return bail(SS_E_OOM);
+  if (cudaMalloc(&c->flag, sizeof(int)) != cudaSuccess) return bail(SS_E_OOM);
+  if (cudaMemsetAsync(c->w, 0, (size_t)c->P_pad * sizeof(float), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->v, 0, (size_t)c->P_pad * sizeof(float), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->w, params, (size_t)n_params * sizeof(float), cudaMemcpyDefault, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return bail(SS_E_CUDA);
+  *out = c;
+  return SS_OK;
+}
+
+ss_status ss_nccl_unique_id(void *out128) {
+  if (!out128) return SS_E_INVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SS_E_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return SS_OK;
+}
+
+ss_status ss_init_dist(ss_ctx *c, int32_t rank, int32_t world, const void *uid) {
+  SS_TRY(check_live(c));
+  if (!uid || world < 1 || rank < 0 || rank >= world) return fail(c, SS_E_INVAL, "bad rank/world");
+  if (c->S % world) return fail(c, SS_E_INVAL, "n_shards (%d) must be a multiple of world (%d)", c->S, world);
+  if (c->stepped || c->comm) return fail(c, SS_E_STATE, "ss_init_dist must precede the first step, once");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof id);
+  SS_NCCL(c, ncclCommInitRank(&c->comm, world, id, rank));
+  c->rank = rank;
+  c->world = world;
+  c->reg_len = c->P_pad / world;
+  c->real_lo.resize(world);
+  c->real_hi.resize(world);
+  for (int32_t r = 0; r < world; ++r) {
+    c->real_lo[r] = std::min<int64_t>((int64_t)r * c->reg_len, c->P);
+    c->real_hi[r] = std::min<int64_t>((int64_t)(r + 1) * c->reg_len, c->P);
+  }
+  // momentum now covers the owned region only
+  float *v = nullptr;
+  SS_CUDA(c, cudaMalloc(&v, (size_t)c->reg_len * sizeof(float)));
+  SS_CUDA(c, cudaMemsetAsync(v, 0, (size_t)c->reg_len * sizeof(float), c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(c->v);
+  c->v = v;
+  return SS_OK;
+}
+
+void ss_destroy(ss_ctx *c) {
+  if (!c) return;
+  if (c->stream) {
+    flush(c);
+    cudaStreamSynchronize(c->stream);
+  }
+  for (auto &t : c->timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (float *p : c->stage) cudaFree(p);
+  for (float *p : c->rslot) cudaFree(p);
+  for (float *p : c->sslot) cudaFree(p);
+  cudaFree(c->sum_buf);
+  cudaFree(c->rs_buf);
+  cudaFree(c->w);
+  cudaFree(c->v);
+  cudaFree(c->flag);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char *ss_last_error(const ss_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+ss_status ss_set_lr_schedule(ss_ctx *c, const int64_t *b, const float *f, int32_t nb) {
+  SS_TRY(check_live(c));
+  if (nb < 0 || nb > kMaxSchedule || (nb > 0 && (!b || !f))) return fail(c, SS_E_INVAL, "bad schedule");
+  for (int32_t i = 0; i < nb; ++i)
+    if (b[i] < 0 || !(f[i] > 0.0f) || (i > 0 && b[i] <= b[i - 1])) return fail(c, SS_E_INVAL, "bad schedule");
+  c->bounds.assign(b, b + nb);
+  c->factors.assign(f, f + nb);
+  return SS_OK;
+}
+
+ss_status ss_set_lr_policy(ss_ctx *c, int32_t asp_rule, float weight_decay) {
+  SS_TRY(check_live(c));
+  if (asp_rule < 0 || asp_rule > 2 || !(weight_decay >= 0.0f)) return fail(c, SS_E_INVAL, "bad lr policy");
+  SS_TRY(flush(c));  // queued pushes keep the lambda they were issued under
+  c->asp_rule = asp_rule;
+  c->lam = weight_decay;
+  return SS_OK;
+}
+
+ss_status ss_current_lr(ss_ctx *c, int32_t proto, float *lr_out) {
+  if (!c || !lr_out || (proto != SS_BSP && proto != SS_ASP)) return SS_E_INVAL;
+  *lr_out = lr_at(c, c->version, proto);
+  return SS_OK;
+}
+
+ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *workers, const int64_t *versions,
+                      int32_t n_local) {
+  SS_TRY(check_live(c));
+  if (!grads || !workers || !versions || n_local < 0) return fail(c, SS_E_INVAL, "null argument");
+  SS_TRY(maybe_switch(c));
+  if (c->proto != SS_BSP) return fail(c, SS_E_STATE, "ss_bsp_step under ASP");
+  // barrier: exactly the expected workers (all n; multi-GPU: this rank's hosted workers), each once
+  std::vector<const float *> by(c->n, nullptr);
+  int32_t expected = 0;
+  for (int32_t j = 0; j < c->n; ++j) expected += host_of(c, j) == c->rank;
+  for (int32_t i = 0; i < n_local; ++i) {
+    const int32_t j = workers[i];
+    if (j < 0 || j >= c->n) return fail(c, SS_E_INVAL, "worker %d out of range", j);
+    if (host_of(c, j) != c->rank) return fail(c, SS_E_PROTOCOL, "worker %d is not hosted on rank %d", j, c->rank);
+    if (by[j] || !grads[i]) return fail(c, SS_E_PROTOCOL, "duplicate or null gradient for worker %d", j);
+    by[j] = grads[i];
+  }
+  if (n_local != expected) return fail(c, SS_E_PROTOCOL, "missing worker: %d of %d gradients", n_local, expected);
+  for (int32_t i = 0; i < n_local; ++i)
+    if (versions[i] != c->version)
+      return fail(c, SS_E_BARRIER, "worker %d base version %lld != current %lld", workers[i],
+                  (long long)versions[i], (long long)c->version);
+  SS_TRY(flush(c));
+  c->stepped = true;
+
+  ss::BspArgs a;
+  std::memset(&a, 0, sizeof a);
+  bool vec = true;
+  int32_t k = 0;
+  for (int32_t j = 0; j < c->n; ++j) {  // ascending worker order (reading C12)
+    if (!by[j]) continue;
+    const float *g = nullptr;
+    SS_TRY(resolve_src(c, by[j], &g));
+    a.g[k++] = g;
+    vec = vec && aligned16(g);
+  }
+  const float eta_t = lr_at(c, c->version, SS_BSP);  // pre-increment version (reading C9)
+  a.flag = c->flag;
+  a.divisor = (float)c->n;
+  a.mu = c->mu;
+  a.neg_eta = -eta_t;
+  a.lam = c->lam;
+  if (c->world == 1) {
+    a.n_in = k;
+    a.w = c->w;
+    a.v = c->v;
+    a.count = c->P;
+    Timed t;
+    timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
+    SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
+    timed_end(c, &t);
+  } else {
+    SS_TRY(ensure_dist_buffers(c));
+    if (k > 0) {
+      ss::SumArgs s;
+      std::memset(&s, 0, sizeof s);
+      for (int32_t i = 0; i < k; ++i) s.g[i] = a.g[i];
+      s.n_in = k;
+      s.out = c->sum_buf;
+      s.count = c->P;
+      s.count_pad = c->P_pad;
+      Timed t;
+      timed_begin(c, &t, 2, 4.0 * ((double)c->P * k + (double)c->P_pad));
+      SS_CUDA(c, ss::launch_local_sum(s, vec, c->stream));
+      timed_end(c, &t);
+    } else {
+      SS_CUDA(c, cudaMemsetAsync(c->sum_buf, 0, (size_t)c->P_pad * sizeof(float), c->stream));
+    }
+    SS_NCCL(c, ncclReduceScatter(c->sum_buf, c->rs_buf, c->reg_len, ncclFloat, ncclSum, c->comm, c->stream));
+    const int64_t lo = c->real_lo[c->rank], cnt = c->real_hi[c->rank] - lo;
+    std::memset(a.g, 0, sizeof a.g);
+    a.g[0] = c->rs_buf;
+    a.n_in = 1;
+    a.w = c->w + lo;
+    a.v = c->v;
+    a.count = cnt;
+    Timed t;
+    timed_begin(c, &t, 0, 4.0 * (double)cnt * 5);
+    SS_CUDA(c, ss::launch_bsp_update(a, true, c->stream));
+    timed_end(c, &t);
+    SS_NCCL(c, ncclAllGather(c->w + (int64_t)c->rank * c->reg_len, c->w, c->reg_len, ncclFloat, c->comm,
+                             c->stream));
+  }
+  c->stage_used = 0;
+  for (int32_t j = 0; j < c->n; ++j) record(c, j, c->version, 0);  // n staleness-0 records
+  c->version += 1;
+  for (auto &b : c->base) b = c->version;
+  return SS_OK;
+}
+
+ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t version, int64_t *staleness_out) {
+  SS_TRY(check_live(c));
+  if (worker < 0 || worker >= c->n) return fail(c, SS_E_INVAL, "worker %d out of range", worker);
+  const bool mine = host_of(c, worker) == c->rank;
+  if (mine && !grad) return fail(c, SS_E_INVAL, "null gradient on the hosting rank");
+  SS_TRY(maybe_switch(c));
+  if (c->proto != SS_ASP) {
+    c->dropped += 1;  // late in-flight push after ASP->BSP
+    return fail(c, SS_E_STATE, "ss_asp_push under BSP (dropped)");
+  }
+  if (version > c->version || version < 0)
+    return fail(c, SS_E_CAUSALITY, "base version %lld > current %lld", (long long)version, (long long)c->version);
+  Ev e{};
+  e.kind = 0;
+  e.worker = worker;
+  if (mine) SS_TRY(resolve_src(c, grad, &e.src));
+  e.lr = lr_at(c, c->version, SS_ASP);
+  const int64_t st = c->version - version;
+  record(c, worker, version, st);
+  c->version += 1;
+  c->stepped = true;
+  if (staleness_out) *staleness_out = st;
+  return enqueue(c, e);
+}
+
+ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
+  SS_TRY(check_live(c));
+  if (worker < 0 || worker >= c->n) return fail(c, SS_E_INVAL, "worker %d out of range", worker);
+  const bool mine = host_of(c, worker) == c->rank;
+  // SPMD rule: at G > 1 every pull moves data, so the hosting rank must name a destination (the others pass NULL
+  // and send their owned slices).
+  if (c->world > 1 && mine && !dst) return fail(c, SS_E_INVAL, "multi-GPU pull needs a destination");
+  SS_TRY(maybe_switch(c));
+  c->base[worker] = c->version;
+  if (version_out) *version_out = c->version;
+  Ev e{};
+  e.kind = 1;
+  e.worker = worker;
+  e.data = c->world > 1 || dst != nullptr;
+  if (!e.data) return SS_OK;
+  if (mine) {
+    if (is_host_ptr(dst)) {
+      float *slot = nullptr;
+      SS_TRY(stage_slot(c, &slot));
+      e.dst = slot;
+      e.host_dst = dst;
+    } else {
+      e.dst = dst;
+    }
+  }
+  return enqueue(c, e);
+}
+
+ss_status ss_switch(ss_ctx *c, int32_t proto, int64_t at_step) {
+  SS_TRY(check_live(c));
+  if (proto != SS_BSP && proto != SS_ASP) return fail(c, SS_E_INVAL, "bad protocol %d", proto);
+  SS_TRY(maybe_switch(c));
+  if (c->has_pending) return fail(c, SS_E_STATE, "a switch is already pending");
+  c->has_pending = true;
+  c->pending_proto = proto;
+  c->pending_at = at_step;
+  return maybe_switch(c);
+}
+
+ss_status ss_asp_replay(ss_ctx *c, const ss_event *ev, int64_t n_ev, int64_t *st_out) {
+  if (!c || (!ev && n_ev > 0) || n_ev < 0) return SS_E_INVAL;
+  for (int64_t i = 0; i < n_ev; ++i) {
+    int64_t r = 0;
+    ss_status s = ev[i].kind == 0 ? ss_asp_push(c, ev[i].worker, ev[i].grad, ev[i].version, &r)
+                                  : ss_pull(c, ev[i].worker, ev[i].dst, &r);
+    if (s != SS_OK) return s;
+    if (st_out) st_out[i] = r;
+  }
+  return SS_OK;
+}
+
+ss_status ss_sync(ss_ctx *c) {
+  SS_TRY(check_live(c));
+  return sync_impl(c);
+}
+
+static ss_status gather_w(ss_ctx *c) {
+  if (c->world == 1) return SS_OK;
+  SS_NCCL(c, ncclAllGather(c->w + (int64_t)c->rank * c->reg_len, c->w, c->reg_len, ncclFloat, c->comm, c->stream));
+  return SS_OK;
+}
+
+ss_status ss_read_params(ss_ctx *c, float *host_dst) {
+  if (!c || !host_dst) return SS_E_INVAL;
+  ss_status s = sync_impl(c);
+  if (s != SS_OK && s != SS_E_DIVERGED) return s;
+  SS_TRY(gather_w(c));
+  SS_CUDA(c, cudaMemcpyAsync(host_dst, c->w, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  return s;
+}
+
+ss_status ss_read_velocity(ss_ctx *c, float *host_dst) {
+  if (!c || !host_dst) return SS_E_INVAL;
+  ss_status s = sync_impl(c);
+  if (s != SS_OK && s != SS_E_DIVERGED) return s;
+  if (c->world == 1) {
+    SS_CUDA(c, cudaMemcpyAsync(host_dst, c->v, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    float *tmp = nullptr;
+    SS_CUDA(c, cudaMallocAsync(&tmp, (size_t)c->P_pad * sizeof(float), c->stream));
+    SS_NCCL(c, ncclAllGather(c->v, tmp, c->reg_len, ncclFloat, c->comm, c->stream));
+    SS_CUDA(c, cudaMemcpyAsync(host_dst, tmp, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    SS_CUDA(c, cudaFreeAsync(tmp, c->stream));
+  }
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  return s;
+}
+
+ss_status ss_get_stats(ss_ctx *c, int64_t *version, int32_t *protocol, uint64_t *hist, int32_t hist_len,
+                       uint64_t *dropped) {
+  if (!c) return SS_E_INVAL;
+  if (!c->diverged) SS_TRY(maybe_switch(c));
+  if (version) *version = c->version;
+  if (protocol) *protocol = c->proto;
+  if (hist)
+    for (int32_t i = 0; i < hist_len; ++i) hist[i] = (size_t)i < c->hist.size() ? c->hist[i] : 0;
+  if (dropped) *dropped = c->dropped;
+  return c->diverged ? SS_E_DIVERGED : SS_OK;
+}
+
+ss_status ss_get_log(ss_ctx *c, int64_t *rec4, int64_t cap, int64_t *total) {
+  if (!c || cap < 0 || (cap > 0 && !rec4)) return SS_E_INVAL;
+  const int64_t nrec = (int64_t)c->log.size() / 4;
+  if (total) *total = nrec;
+  const int64_t m = cap < nrec ? cap : nrec;
+  if (m > 0) std::memcpy(rec4, c->log.data(), (size_t)m * 4 * sizeof(int64_t));
+  return SS_OK;
+}
+
+ss_status ss_set_window(ss_ctx *c, int32_t max_events) {
+  SS_TRY(check_live(c));
+  if (max_events < 1 || max_events > ss::kMaxEvents) return fail(c, SS_E_INVAL, "window must be in [1, 64]");
+  SS_TRY(flush(c));
+  c->max_win = max_events;
+  return SS_OK;
+}
+
+ss_status ss_get_stream(ss_ctx *c, void **s) {
+  if (!c || !s) return SS_E_INVAL;
+  *s = c->stream;
+  return SS_OK;
+}
+
+ss_status ss_wait_stream(ss_ctx *c, void *stream) {
+  if (!c) return SS_E_INVAL;
+  cudaEvent_t e;
+  SS_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  SS_CUDA(c, cudaEventRecord(e, (cudaStream_t)stream));
+  SS_CUDA(c, cudaStreamWaitEvent(c->stream, e, 0));
+  cudaEventDestroy(e);
+  return SS_OK;
+}
+
+ss_status ss_profile(ss_ctx *c, int32_t on) {
+  if (!c) return SS_E_INVAL;
+  SS_TRY(drain_timed(c));
+  c->prof = on != 0;
+  if (on)
+    for (auto &k : c->kstat) k = KStat{};
+  return SS_OK;
+}
+
+ss_status ss_kernel_stats(ss_ctx *c, int32_t id, int64_t *launches, double *ms, double *bytes) {
+  if (!c || id < 0 || id > 2) return SS_E_INVAL;
+  SS_TRY(drain_timed(c));
+  if (launches) *launches = c->kstat[id].launches;
+  if (ms) *ms = c->kstat[id].ms;
+  if (bytes) *bytes = c->kstat[id].bytes;
+  return SS_OK;
+}
+
+ss_status ss_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst, void *stream) {
+  if (!dst || j < 0 || j > 255 || k < 0 || k >= (int64_t(1) << 26) || i0 < 0 || count < 0 ||
+      i0 + count > (int64_t(1) << 30))
+    return SS_E_INVAL;
+  return ss::launch_synth_grad(seed, j, k, i0, count, dst, (cudaStream_t)stream) == cudaSuccess ? SS_OK : SS_E_CUDA;
+}
+
+ss_status ss_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                          float *grad, float *loss, void *stream) {
+  if (!X || !y || !W || !grad || !loss || B < 1 || B > 1024 || d < 1 || C < 1 || C > 32) return SS_E_INVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  float *scratch = nullptr;
+  if (cudaMallocAsync(&scratch, (size_t)B * (C + 1) * sizeof(float), s) != cudaSuccess) return SS_E_OOM;
+  cudaError_t e = ss::launch_softmax_grad(X, y, B, d, C, W, grad, loss, scratch, s);
+  cudaFreeAsync(scratch, s);
+  return e == cudaSuccess ? SS_OK : SS_E_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,411 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Single GPU: the reduction order is fixed on both sides (ascending workers, explicit FMA; reading C12), so
+parameters, momentum and pull snapshots must be BIT-identical, and every protocol integer (version, staleness,
+applied order, histogram, dropped count) exact. The toy model's gradient kernel (exp/log in fp32 vs the oracle's
+fp64) is compared with the C13 tolerance |x - y| <= 1e-5 |y| + 1e-5 rms(y).
+"""
+import collections
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SEED = 20241018
+BSP, ASP = 0, 1
+
+
+@pytest.fixture(scope="module")
+def ss():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2104_08364_b200 import build
+    build.build()
+    from paper_2104_08364_b200 import syncswitch
+    torch.cuda.init()
+    return syncswitch
+
+
+def dev_synth(ss, j, k, P, seed=SEED, offset=0):
+    buf = torch.empty(P + offset, dtype=torch.float32, device="cuda")
+    out = buf[offset:]
+    assert ss.ss_synth_grad(seed, j, k, 0, P, out) == 0
+    torch.cuda.synchronize()
+    return out
+
+
+def host_synth(orc, j, k, P, seed=SEED):
+    return orc.synth_grad(seed, j, k, 0, P)
+
+
+def init_params(orc, P):
+    return orc.synth_grad(SEED + 1, 255, 0, 0, P) * 64.0   # uniform in [-0.5, 0.5), exact in fp32
+
+
+def close_c13(x, y, rel=1e-5):
+    x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+    rms = np.sqrt(np.mean(y * y)) if y.size else 0.0
+    return np.all(np.abs(x - y) <= rel * np.abs(y) + rel * rms)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("j,k,i0,count,offset", [(0, 0, 0, 1, 0), (3, 5, 1000, 4099, 0), (255, 2 ** 26 - 1, 7, 333, 1),
+                                                 (7, 12, 2 ** 30 - 4096, 4096, 2)])
+def test_synth_grad_bit_exact(ss, orc, j, k, i0, count, offset):
+    buf = torch.zeros(count + offset, dtype=torch.float32, device="cuda")
+    assert ss.ss_synth_grad(SEED, j, k, i0, count, buf[offset:]) == 0
+    got = buf[offset:].cpu().numpy()
+    assert np.array_equal(got, orc.synth_grad(SEED, j, k, i0, count))
+
+
+# ---------------------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("P,n,S", [(1, 1, 1), (7, 2, 3), (1000, 3, 2), (100003, 8, 8), (464154, 8, 8),
+                                   (5000, 11, 4), (4096, 16, 16)])
+@pytest.mark.parametrize("lam", [0.0, 1e-4])
+def test_bsp_bit_exact(ss, orc, P, n, S, lam):
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.05, 0.9)
+    o = orc.Oracle(w0, S, n, 0.05, 0.9)
+    for x in (g, o):
+        x.set_lr_schedule([2], [0.1])        # a decay boundary inside the run (version coordinate)
+        x.set_lr_policy(0, lam)
+    for step in range(3):
+        dg = [dev_synth(ss, j, step, P) for j in range(n)]
+        hg = [host_synth(orc, j, step, P) for j in range(n)]
+        perm = list(reversed(range(n)))       # order of submission must not matter (sum is ascending by id)
+        g.bsp_step([dg[j] for j in perm], perm, [step] * n)
+        assert o.bsp_step(hg) == 0
+    assert np.array_equal(g.params(), o.params())
+    assert np.array_equal(g.velocity(), o.velocity())
+    sg, so = g.stats(), o.stats()
+    assert sg["version"] == so["version"] == 3 and np.array_equal(sg["hist"], so["hist"])
+    assert np.array_equal(g.log(), o.log())
+    g.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def run_asp_pair(ss, orc, P, n, S, kind, worker, window, host_buffers=False, offset=0, lam=0.0):
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for x in (g, o):
+        x.set_lr_schedule([60], [0.5])
+        x.set_lr_policy(0, lam)
+        x.switch(ASP, 0)
+    g.set_window(window)
+    base_g, base_o = {}, {}
+    pulls_g, pulls_o, st_g, st_o = [], [], [], []
+    keep = []
+    pushes = collections.Counter()
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            if host_buffers:
+                dst = np.empty(P, np.float32)
+            else:
+                dst = torch.empty(P + offset, dtype=torch.float32, device="cuda")[offset:]
+            base_g[j] = g.pull(j, dst)
+            rc, snap, base_o[j] = o.pull(j)
+            pulls_g.append(dst)
+            pulls_o.append(snap)
+        else:
+            k = pushes[j]
+            pushes[j] += 1
+            if host_buffers:
+                grad = host_synth(orc, j, k, P)
+            else:
+                grad = dev_synth(ss, j, k, P, offset=offset)
+            keep.append(grad)                  # borrowed until sync
+            st_g.append(g.asp_push(j, grad, base_g[j]))
+            rc, s = o.asp_push(j, host_synth(orc, j, k, P), base_o[j])
+            assert rc == 0
+            st_o.append(s)
+    g.sync()
+    return g, o, pulls_g, pulls_o, st_g, st_o
+
+
+@pytest.mark.parametrize("window", [1, 7, 16, 64])
+@pytest.mark.parametrize("P,S", [(10007, 4), (4096, 1)])
+def test_asp_bit_exact(ss, orc, window, P, S):
+    n = 4
+    kind, worker, tick = orc.schedule(n, [1000, 1100, 1300, 1700], 120, jitter=100, seed=7)
+    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, S, kind, worker, window)
+    assert sg == so and max(so) > 0
+    for a, b in zip(pg, po):
+        assert np.array_equal(a.cpu().numpy(), b)          # every snapshot sees exactly the pushes before it
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert np.array_equal(g.log(), o.log())
+    assert np.array_equal(g.stats()["hist"], o.stats()["hist"])
+    g.close()
+
+
+def test_asp_host_buffers_and_weight_decay(ss, orc):
+    n, P = 3, 3001
+    kind, worker, _ = orc.schedule(n, [1000] * n, 40, jitter=100, seed=3)
+    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, 2, kind, worker, 16, host_buffers=True, lam=1e-3)
+    assert sg == so
+    for a, b in zip(pg, po):
+        assert np.array_equal(a, b)
+    assert np.array_equal(g.params(), o.params())
+    g.close()
+
+
+def test_asp_unaligned_scalar_path(ss, orc):
+    n, P = 2, 2053
+    kind, worker, _ = orc.schedule(n, [1000, 1500], 30, jitter=0)
+    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, 1, kind, worker, 8, offset=1)
+    for a, b in zip(pg, po):
+        assert np.array_equal(a.cpu().numpy(), b)
+    assert np.array_equal(g.params(), o.params())
+    g.close()
+
+
+def test_straggler_histogram_on_gpu(ss, orc):
+    # config 4 shape (SURVEY §8c pin): the staleness integers through the C-ABI match the brute-force pin
+    n, P = 8, 64
+    kind, worker, _ = orc.schedule(n, [1000] * 7 + [4000], 3000)
+    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, 8, kind, worker, 64)
+    assert sg == so
+    assert collections.Counter(sg)[28] == collections.Counter(so)[28] > 0
+    assert np.array_equal(g.params(), o.params())
+    g.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def test_switch_bsp_asp_bsp_bit_exact(ss, orc):
+    n, S, P = 4, 4, 9999
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for x in (g, o):
+        x.set_lr_schedule([5, 9], [0.1, 0.01])
+    k = collections.Counter()
+
+    def grads(js):
+        out_d, out_h = [], []
+        for j in js:
+            out_d.append(dev_synth(ss, j, k[j], P))
+            out_h.append(host_synth(orc, j, k[j], P))
+            k[j] += 1
+        return out_d, out_h
+
+    keep = []
+    for step in range(3):
+        d, h = grads(range(n))
+        keep += d
+        g.bsp_step(d)
+        assert o.bsp_step(h) == 0
+    assert g.switch_status(ASP, 3) == o.switch(ASP, 3) == 0
+    assert g.stats()["protocol"] == o.stats()["protocol"] == ASP
+    dst_g = {j: torch.empty(P, device="cuda") for j in range(n)}
+    bg = {j: g.pull(j, dst_g[j]) for j in range(n)}
+    bo = {j: o.pull(j)[2] for j in range(n)}
+    for j in (2, 0, 3):                               # three pushes land, worker 1's stays in flight
+        d, h = grads([j])
+        keep += d
+        assert g.asp_push(j, d[0], bg[j]) == o.asp_push(j, h[0], bo[j])[1]
+    assert g.switch_status(BSP, 0) == o.switch(BSP, 0) == 0
+    d, h = grads([1])
+    assert g.asp_push_status(1, d[0], bg[1])[0] == o.asp_push(1, h[0], bo[1])[0] == 2   # dropped
+    assert g.stats()["dropped"] == o.stats()["dropped"] == 1
+    assert g.version == o.version == 6
+    for step in range(4):                             # across the decay boundaries at 9
+        d, h = grads(range(n))
+        keep += d
+        g.bsp_step(d, versions=[6 + step] * n)
+        assert o.bsp_step(h, versions=[6 + step] * n) == 0
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert np.array_equal(g.log(), o.log())
+    g.close()
+
+
+def test_switch_fraction_endpoints_on_gpu(ss, orc):
+    # s = 1 (switch beyond the run) == pure BSP;  s = 0 == pure ASP — on the device path
+    n, S, P = 2, 2, 4099
+    w0 = init_params(orc, P)
+    a = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    b = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    b.switch(ASP, 4)
+    keep = []
+    for step in range(4):
+        gs = [dev_synth(ss, j, step, P) for j in range(n)]
+        keep += gs
+        a.bsp_step(gs)
+        b.bsp_step(gs)
+    assert np.array_equal(a.params(), b.params())
+    assert b.stats()["protocol"] == ASP
+    a.close()
+    b.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def test_errors_match_oracle(ss, orc):
+    P, n = 64, 2
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), 1, n, 0.1, 0.9)
+    o = orc.Oracle(w0, 1, n, 0.1, 0.9)
+    x = dev_synth(ss, 0, 0, P)
+    h = host_synth(orc, 0, 0, P)
+    assert g.bsp_step_status([x]) == o.bsp_step([h]) == ss.SS_E_PROTOCOL
+    assert g.bsp_step_status([x, x], [1, 1]) == o.bsp_step([h, h], workers=[1, 1]) == ss.SS_E_PROTOCOL
+    assert g.bsp_step_status([x, x], [0, 1], [0, 1]) == o.bsp_step([h, h], versions=[0, 1]) == ss.SS_E_BARRIER
+    assert g.asp_push_status(0, x, 0)[0] == o.asp_push(0, h, 0)[0] == ss.SS_E_STATE
+    assert g.version == o.version == 0
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    assert g.bsp_step_status([x, x]) == o.bsp_step([h, h]) == ss.SS_E_STATE
+    assert g.asp_push_status(0, x, 3)[0] == o.asp_push(0, h, 3)[0] == ss.SS_E_CAUSALITY
+    assert g.asp_push_status(5, x, 0)[0] == o.asp_push(5, h, 0)[0] == ss.SS_E_INVAL
+    assert g.switch_status(BSP, 10) == o.switch(BSP, 10) == 0
+    assert g.switch_status(ASP, 20) == o.switch(ASP, 20) == ss.SS_E_STATE
+    assert g.stats()["dropped"] == o.stats()["dropped"] == 1
+    g.close()
+
+
+def test_divergence_is_sticky(ss, orc):
+    P = 1000
+    g = ss.SyncSwitch(torch.zeros(P, device="cuda"), 2, 1, 0.1, 0.9)
+    bad = torch.zeros(P, device="cuda")
+    bad[17] = float("nan")
+    g.bsp_step([bad])
+    assert g.sync_status() == ss.SS_E_DIVERGED
+    assert g.bsp_step_status([bad]) == ss.SS_E_DIVERGED
+    assert g.switch_status(ASP, 0) == ss.SS_E_DIVERGED
+    g.close()
+    g = ss.SyncSwitch(torch.zeros(P, device="cuda"), 2, 1, 0.1, 0.9)
+    g.switch(ASP, 0)
+    inf = torch.zeros(P, device="cuda")
+    inf[999] = float("inf")
+    g.asp_push(0, inf, 0)
+    assert g.sync_status() == ss.SS_E_DIVERGED
+    g.close()
+
+
+def test_repeated_init_destroy(ss):
+    for _ in range(20):
+        g = ss.SyncSwitch(torch.zeros(1 << 16, device="cuda"), 4, 4, 0.1, 0.9)
+        g.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def test_full_size_config3_sampled(ss, orc):
+    """BASELINE config 3 at full size (P = 25,557,032, n = S = 8), in the bench's launch configuration (window 16):
+    oracle checked on 4,096 sampled elements — the update is elementwise, so an oracle built on those indices only
+    (shard invariance) is exact for them."""
+    from inputs import RESNET50_P
+    P, n, S = RESNET50_P, 8, 8
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.choice(P, 4090, replace=False), [0, 1, P - 2, P - 1]]))
+    w0d = torch.empty(P, device="cuda")
+    ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0d)
+    w0d *= 64.0
+    g = ss.SyncSwitch(w0d, S, n, 0.1, 0.9)
+    g.set_window(16)
+    w0s = np.array([orc.synth_grad(SEED + 1, 255, 0, int(i), 1)[0] * 64.0 for i in idx], np.float32)
+    o = orc.Oracle(w0s, 1, n, 0.1, 0.9)
+
+    def sample(j, k):
+        return np.array([orc.synth_grad(SEED, j, k, int(i), 1)[0] for i in idx], np.float32)
+
+    grads = [dev_synth(ss, j, 0, P) for j in range(n)]
+    g.bsp_step(grads)
+    o.bsp_step([sample(j, 0) for j in range(n)])
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    snaps = [torch.empty(P, device="cuda") for _ in range(n)]
+    for j in range(n):
+        g.pull(j, snaps[j])
+        o.pull(j, False)
+    for j in range(n):                               # one round: 8 pushes then 8 pulls (k = 1 ring slot)
+        grads[j] = dev_synth(ss, j, 1, P)
+        assert g.asp_push(j, grads[j], 1) == j
+        assert o.asp_push(j, sample(j, 1), 1) == (0, j)
+        g.pull(j, snaps[j])
+    g.sync()
+    wg = g.params()
+    assert np.array_equal(wg[idx], o.params())
+    assert np.array_equal(g.velocity()[idx], o.velocity())
+    ti = torch.from_numpy(idx).cuda()
+    assert np.array_equal(snaps[n - 1][ti].cpu().numpy(), o.params())
+    g.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+def test_softmax_grad_kernel(ss, orc):
+    from inputs import toy_dataset
+    X, y = toy_dataset(seed=1, n_points=64)
+    B, d, C = 16, X.shape[1], 8
+    rng = np.random.default_rng(0)
+    W = (rng.standard_normal(d * C) * 0.01).astype(np.float32)
+    Xd, yd, Wd = torch.from_numpy(X[:B]).cuda(), torch.from_numpy(y[:B]).cuda(), torch.from_numpy(W).cuda()
+    grad = torch.empty(d * C, device="cuda")
+    loss = torch.empty(1, device="cuda")
+    assert ss.ss_softmax_grad(Xd, yd, B, d, C, Wd, grad, loss) == 0
+    lo, go = orc.softmax_loss_grad(X[:B], y[:B], W.astype(np.float64))
+    assert close_c13(grad.cpu().numpy(), go) and abs(loss.item() - lo) <= 1e-5 * abs(lo)
+    # zero parameters: loss = ln C exactly up to fp32 rounding
+    assert ss.ss_softmax_grad(Xd, yd, B, d, C, torch.zeros(d * C, device="cuda"), grad, loss) == 0
+    assert loss.item() == pytest.approx(np.log(C), rel=1e-6)
+
+
+def test_config1_toy_end_to_end(ss, orc):
+    """Config 1: 2 workers, 2 shards, softmax regression on 1,000 points (P = 8,192), W = 100 B samples, switch
+    BSP -> ASP at s = 0.5 (25 BSP steps + 50 ASP pushes, Table I arithmetic), seeded jittered schedule. Each side
+    computes its own gradients from its own pulls (GPU: softmax_grad kernel fp32; oracle: fp64)."""
+    from inputs import minibatch_order, toy_dataset
+    n, S, B, d, C = 2, 2, 16, 1024, 8
+    X, y = toy_dataset(seed=1)
+    bsp_steps, asp_pushes, _ = orc.table1(100 * B, B, n, 1, 2, [])
+    assert (bsp_steps, asp_pushes) == (25, 50)
+    order = minibatch_order(1, len(X), n * bsp_steps + asp_pushes, B)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    P = d * C
+    g = ss.SyncSwitch(torch.zeros(P, device="cuda"), S, n, 0.1, 0.9)
+    o = orc.Oracle(np.zeros(P, np.float32), S, n, 0.1, 0.9)
+    for x in (g, o):
+        x.switch(ASP, bsp_steps)
+    loss = torch.empty(1, device="cuda")
+    mb = iter(range(len(order)))
+
+    def gpu_grad(Wdev, batch):
+        bi = torch.from_numpy(order[batch]).cuda()
+        gr = torch.empty(P, device="cuda")
+        assert ss.ss_softmax_grad(Xd[bi].contiguous(), yd[bi].contiguous(), B, d, C, Wdev, gr, loss) == 0
+        return gr
+
+    def orc_grad(Wh, batch):
+        return orc.softmax_loss_grad(X[order[batch]], y[order[batch]], Wh.astype(np.float64))[1].astype(np.float32)
+
+    wdev = torch.empty(P, device="cuda")
+    losses = []
+    for step in range(bsp_steps):
+        batches = [next(mb) for _ in range(n)]
+        g.pull(0, wdev)
+        g.sync()
+        g.bsp_step([gpu_grad(wdev, b) for b in batches])
+        losses.append(loss.item())
+        wo = o.params()
+        assert o.bsp_step([orc_grad(wo, b) for b in batches]) == 0
+    kind, worker, _ = orc.schedule(n, [1000] * n, asp_pushes, jitter=100, seed=7)
+    snap_g = {j: torch.empty(P, device="cuda") for j in range(n)}
+    snap_o, base_g, base_o = {}, {}, {}
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            base_g[j] = g.pull(j, snap_g[j])
+            _, snap_o[j], base_o[j] = o.pull(j)
+            g.sync()
+        else:
+            b = next(mb)
+            sg = g.asp_push(j, gpu_grad(snap_g[j], b), base_g[j])
+            g.sync()
+            losses.append(loss.item())
+            rc, so = o.asp_push(j, orc_grad(snap_o[j], b), base_o[j])
+            assert rc == 0 and sg == so
+    assert g.version == o.version == bsp_steps + asp_pushes
+    assert np.array_equal(g.log(), o.log())
+    assert close_c13(g.params(), o.params())
+    assert np.mean(losses[-10:]) < 0.5 * losses[0]       # it trains
+    g.close()
