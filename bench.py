@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the Sync-Switch synchronization path on B200 (BASELINE.json metric: BSP sync steps/s and ASP pushes/s
+at 1/2/4/8 B200; HBM & NVLink GB/s vs peak).
+
+One bench STEP is one pass of the whole hot path over one batch of synthetic gradients:
+  BSP superstep (n gradients: barrier, aggregate, momentum update, broadcast)  -> in-place switch to ASP
+  -> one ASP round (n pushes, each followed by the pusher's pull; staleness 0..n-1) -> in-place switch back to BSP.
+Workload at N=1 and by default: BASELINE config 3 (ResNet-50-shaped, P = 25,557,032 fp32, n = S = 8). Gradients
+come from the seeded synth_grad kernel into per-worker rings (2 slots) before timing; the step streams ~3.3 GB,
+far above the 126 MB L2, so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|2|5a..5d] [--impl ours|reference]
+N > 1: launched by torchrun; one process per GPU, NCCL over NVLink (reduce-scatter / all-gather for BSP,
+owner-routed send/recv for ASP); strong scaling (P and n fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "3": dict(P=25_557_032, n=8, S=8, window=16, name="config3: ResNet-50-shaped sync, P=25,557,032 fp32, "
+                                                        "n=8 workers, S=8 shards"),
+    "2": dict(P=464_154, n=8, S=8, window=16, name="config2: ResNet-32/CIFAR-10-shaped sync, P=464,154 fp32, "
+                                                     "n=8 workers, S=8 shards"),
+    "5a": dict(P=100_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=1e8 fp32, n=S=8"),
+    "5b": dict(P=250_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=2.5e8 fp32, n=S=8"),
+}
+METRIC = "BSP sync steps/s and ASP pushes/s at 1/2/4/8 B200; HBM & NVLink GB/s vs peak"
+UNIT = "steps/s (1 step = 1 BSP superstep + switch + n ASP push/pull + switch)"
+SEED = 20241018
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2104_08364_b200 import syncswitch as ss
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    P, n, S, win = cfg["P"], cfg["n"], cfg["S"], cfg["window"]
+    hosted = [j for j in range(n) if (j * world) // n == rank]
+
+    # initial parameters (seeded, identical on every rank) and the context
+    w0 = torch.empty(P, device="cuda")
+    ss.ss_check(ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0))
+    w0.mul_(64.0)
+    torch.cuda.synchronize()
+    g = ss.SyncSwitch(w0, S, n, 0.1, 0.9)
+    if world > 1:
+        uid = [ss.ss_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        g.init_dist(rank, world, uid[0])
+    g.set_window(win)
+    del w0
+
+    # gradient rings: slot 0 feeds the BSP superstep, slot 1 the ASP round
+    ring = {(j, r): torch.empty(P, device="cuda") for j in hosted for r in range(2)}
+    for (j, r), buf in ring.items():
+        ss.ss_check(ss.ss_synth_grad(SEED, j, r, 0, P, buf))
+    pull_dst = {j: torch.empty(P, device="cuda") for j in hosted}
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(g.stream)
+
+    def step(grad_src, dst_src):
+        ver = g.version
+        g.bsp_step([grad_src[(j, 0)] for j in hosted], hosted, [ver] * len(hosted))
+        g.switch(ss.SS_ASP, 0)
+        base = ver + 1
+        for j in range(n):
+            st = g.asp_push(j, grad_src.get((j, 1)), base)
+            assert st == j
+            g.pull(j, dst_src.get(j))
+        g.switch(ss.SS_BSP, 0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(ring, pull_dst)
+    barrier()
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    g.profile(True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
+    barrier()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        ver = g.version
+        g.bsp_step([ring[(j, 0)] for j in hosted], hosted, [ver] * len(hosted))
+        ev[2 * k + 1].record(stream)
+        g.switch(ss.SS_ASP, 0)
+        for j in range(n):
+            g.asp_push(j, ring.get((j, 1)), ver + 1)
+            g.pull(j, pull_dst.get(j))
+        g.switch(ss.SS_BSP, 0)
+        g.stats(1)                     # resolves the switch back (flushes the ASP window) inside the step
+        ev[2 * k + 2].record(stream)
+    barrier()
+    clk = clocks.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    bsp_ms = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
+    asp_ms = sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(args.steps))
+    kst = {name: g.kernel_stats(i) for i, name in enumerate(["bsp_update", "asp_replay", "local_sum"])}
+    g.profile(False)
+    t = torch.tensor([total_ms, bsp_ms, asp_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, bsp_ms, asp_ms = t.tolist()
+    launches = sum(k["launches"] for k in kst.values())
+
+    st = g.stats(64)
+    assert st["status"] == 0 and g.sync_status() == 0, g.last_error()
+
+    # e2e: same steps through the C-ABI with HOST (pinned) buffers, H2D / D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hring = {(j, r): torch.empty(P, pin_memory=True) for j in hosted for r in range(2)}
+        for key, buf in hring.items():
+            buf.copy_(ring[key])
+        hdst = {j: torch.empty(P, pin_memory=True) for j in hosted}
+        del ring
+        torch.cuda.empty_cache()
+        step(hring, hdst)
+        g.sync()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            step(hring, hdst)
+            g.sync()                   # the step's results (pull snapshots) are on the host
+        e1.record(stream)
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = 4 * P * 2 * len(hosted)
+        d2h = 4 * P * len(hosted)
+        e2e = {"value": args.e2e_steps / (et.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "note": "pinned host gradients and pull destinations, copies staged by the library"}
+
+    hbm_peak, peak_src = peaks()
+    # dominant kernel by device time
+    dom = max(("bsp_update", "asp_replay"), key=lambda k: kst[k]["ms"])
+    d = kst[dom]
+    achieved = (d["bytes"] / d["launches"]) / (d["ms"] / d["launches"] / 1e3) / 1e9 if d["launches"] else 0.0
+    traffic = ncu_traffic(dom, args.config)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                "avg_launch_us": 1e3 * d["ms"] / max(d["launches"], 1), "peak_source": peak_src,
+                "frac_of_nominal_8TBps": round(achieved / 8000.0, 4)}
+    kernels = {}
+    for name, k in kst.items():
+        if k["launches"]:
+            gbs = k["bytes"] / (k["ms"] / 1e3) / 1e9
+            kernels[name] = {"launches": k["launches"], "avg_us": round(1e3 * k["ms"] / k["launches"], 2),
+                             "GBps": round(gbs, 1), "frac": round(gbs / hbm_peak, 4),
+                             "share_of_step": round(k["ms"] / (total_ms * (1 if world == 1 else 1)), 4)}
+
+    steps_per_s = args.steps / (total_ms / 1e3)
+    phases = {"bsp_steps_per_s": args.steps / (bsp_ms / 1e3), "asp_pushes_per_s": n * args.steps / (asp_ms / 1e3),
+              "bsp_ms_per_step": bsp_ms / args.steps, "asp_ms_per_round": asp_ms / args.steps}
+    if world > 1:
+        # NCCL bus bandwidth convention for the BSP exchange: RS + AG each move (G-1)/G * 4 P_pad per GPU
+        P_pad = S * (((P + S - 1) // S + 31) // 32 * 32)
+        per_dir = 2 * (world - 1) / world * 4 * P_pad
+        phases["bsp_nvlink_busbw_GBps"] = per_dir / (bsp_ms / args.steps / 1e3) / 1e9
+        phases["bsp_nvlink_frac_of_900"] = phases["bsp_nvlink_busbw_GBps"] / 900.0
+        phases["bsp_nvlink_frac_of_770_measured"] = phases["bsp_nvlink_busbw_GBps"] / 770.0
+    line = {
+        "metric": METRIC, "value": round(steps_per_s, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash gradients)",
+        "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "asp_window_events": win,
+                   "parallelism": f"sharded PS over {world} GPU(s)",
+                   "l2": "inputs larger than L2 (~3.3 GB streamed per step vs 126 MB L2), no flush"},
+        "phases": phases, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
+        "e2e": e2e,
+        "protocol_check": {"version": st["version"], "hist_0_to_n": [int(x) for x in st["hist"][:n + 1]]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        del g
+        torch.cuda.empty_cache()
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+    g = None
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------------------------------
+def _oracle_step(orc, o, n, grads_bsp, grads_asp):
+    ver = o.version
+    assert o.bsp_step(grads_bsp, versions=[ver] * n) == 0
+    o.switch(orc.ASP, 0)
+    for j in range(n):
+        rc, st = o.asp_push(j, grads_asp[j], ver + 1)
+        assert rc == 0 and st == j
+        o.pull(j)
+    o.switch(orc.BSP, 0)
+
+
+def _oracle_inputs(orc, n, P):
+    import numpy as np
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    gb = [orc.synth_grad(SEED, j, 0, 0, P) for j in range(n)]
+    ga = [orc.synth_grad(SEED, j, 1, 0, P) for j in range(n)]
+    return w0, gb, ga
+
+
+def cpu_baseline(cfg, seconds: float):
+    """The oracle as it stands (single-threaded C), on this host, on a bounded sample: full-size steps until
+    `seconds` of CPU work (at least one)."""
+    import oracle as orc
+    orc.build()
+    P, n, S = cfg["P"], cfg["n"], cfg["S"]
+    w0, gb, ga = _oracle_inputs(orc, n, P)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        _oracle_step(orc, o, n, gb, ga)
+        k += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": k / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{k} full-size steps of the same workload ({el:.1f} s, P={P}, n={n})",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host's cores, on the same config / metric / unit. Each step is
+    the same step on a bounded sample: the first P_s elements of the parameter vector (the path is elementwise, cost
+    linear in P), with P_s sized so the K + W steps take ~2 minutes; value = full-workload steps/s."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and rank != 0:
+        return
+    import oracle as orc
+    orc.build()
+    cfg = CONFIGS[args.config]
+    P, n, S = cfg["P"], cfg["n"], cfg["S"]
+    # calibrate on a 1M-element slice
+    Pc = min(P, 1 << 20)
+    w0, gb, ga = _oracle_inputs(orc, n, Pc)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    t0 = time.perf_counter()
+    _oracle_step(orc, o, n, gb, ga)
+    per_elem = (time.perf_counter() - t0) / Pc
+    budget = 120.0 / max(args.steps + args.warmup, 1)
+    Ps = int(max(4096, min(P, budget / per_elem)))
+    w0, gb, ga = _oracle_inputs(orc, n, Ps)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for _ in range(args.warmup):
+        _oracle_step(orc, o, n, gb, ga)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _oracle_step(orc, o, n, gb, ga)
+    el = time.perf_counter() - t0
+    value = args.steps / el * (Ps / P)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash gradients)",
+            "impl": "reference",
+            "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step on the first {Ps} of {P} elements ({Ps / P:.4f} of the vector), "
+                                       f"scaled by P/P_s"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
