@@ -201,7 +201,7 @@ def run_ours(args):
     total_ms = ev[0].elapsed_time(ev[-1])
     bsp_ms = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
     asp_ms = sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(args.steps))
-    kst = {name: g.kernel_stats(i) for i, name in enumerate(["bsp_update", "asp_replay", "local_sum"])}
+    kst = {name: g.kernel_stats(i) for i, name in enumerate(["bsp_update", "asp_replay", "local_sum", "scatter"])}
     g.profile(False)
     t = torch.tensor([total_ms, bsp_ms, asp_ms], dtype=torch.float64, device="cuda")
     if world > 1:

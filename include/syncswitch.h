@@ -74,6 +74,20 @@ ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n
  * (already stepped or already distributed), SS_E_NCCL. */
 ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *nccl_unique_id);
 
+/* Multi-GPU exchange implementation (collective; every rank passes the same mode):
+ *   0  NCCL: BSP = local pre-sum -> ncclReduceScatter -> owner bsp_update -> ncclAllGather; ASP windows = grouped
+ *      ncclSend/ncclRecv of gradient slices to owners and snapshot slices to pullers.
+ *   1  fused peer memory, exact (default): CUDA-IPC-mapped buffers over NVLink/NVSwitch. A scatter kernel stores each
+ *      hosted gradient's owner slices into the owners' inboxes; the owner kernel sums the n worker slices in
+ *      ascending worker order (bit-identical to the single-GPU result), updates w and v, and stores the new slice into
+ *      every rank's replica (BSP) or each pull's snapshot slice into the puller's buffer (ASP). Cross-GPU ordering by
+ *      release/acquire flags inside the kernels (bounded waits: a missing peer yields SS_E_CUDA at ss_sync, never a
+ *      hang). At most 8 ranks.
+ *   2  fused peer memory, pre-summed: as 1, but each rank first sums its hosted workers and sends one slice per
+ *      owner (fewer NVLink bytes when n > world; summation order: ascending within a rank, then ascending ranks).
+ * Errors: SS_E_INVAL. */
+ss_status ss_set_fused(ss_ctx *ctx, int32_t mode);
+
 /* Fills the 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
 ss_status ss_nccl_unique_id(void *out128);
 
@@ -176,7 +190,7 @@ ss_status ss_get_stream(ss_ctx *ctx, void **stream_out);
 ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
 /* Kernel timing: when on, every bsp_update / asp_replay launch is bracketed by CUDA events on the context's stream;
  * ss_kernel_stats returns per-kernel launch count, total device milliseconds and algorithmic HBM bytes
- * (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum). Reading synchronizes. */
+ * (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum, 3 = scatter). Reading synchronizes. */
 ss_status ss_profile(ss_ctx *ctx, int32_t on);
 ss_status ss_kernel_stats(ss_ctx *ctx, int32_t kernel_id, int64_t *launches, double *total_ms, double *bytes);
 

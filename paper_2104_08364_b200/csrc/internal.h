@@ -7,6 +7,21 @@ namespace ss {
 
 constexpr int kMaxWorkers = 256;  // SV §8b: workers in [1, 256]
 constexpr int kMaxEvents = 64;    // events per ASP replay window
+constexpr int kMaxPeers = 8;      // GPUs of one NVSwitch box
+
+// Cross-GPU flag barrier over CUDA-IPC-mapped peer memory (fused path). Every rank owns
+// sig_local[kMaxPeers] (written remotely by peers at index [their rank]) and a CTA completion counter. Epochs grow
+// monotonically on every rank in the same SPMD order, so no flag is ever reset.
+struct PeerSync {
+  uint32_t *sig_local;              // this GPU's inbound flags
+  uint32_t *sig_peer[kMaxPeers];    // rank q's sig_local (mapped; [rank] == sig_local)
+  uint32_t *ctr;                    // CTA completion counter (local, returns to 0 after each use)
+  int *err;                         // set when a wait times out (surfaced by ss_sync as SS_E_CUDA)
+  int32_t rank, world;
+  uint32_t wait_epoch;              // !=0: every CTA waits for flag >= wait_epoch from all ranks before starting
+  uint32_t signal_epoch;            // !=0: the last CTA to finish signals every rank with signal_epoch
+  int32_t end_wait;                 // and then waits until every rank has signalled signal_epoch
+};
 
 // bsp_update (SV §2.5 K1): out-of-place aggregate of n_in inputs in ascending order, mean by `divisor`,
 // momentum update of the owner slice. 1-GPU form: inputs = the n worker gradients, divisor = n. Post-reduce-scatter
@@ -22,6 +37,9 @@ struct BspArgs {
   float mu;
   float neg_eta;
   float lam;
+  float *bcast[kMaxPeers];  // fused path: remote replicas (at this slice's offset) that receive the updated w
+  int32_t n_bcast;
+  PeerSync sync;
 };
 
 // local_sum: out[i] = sum_{j ascending} g[j][i] for i < count, 0 for count <= i < count_pad (multi-GPU pre-sum
@@ -50,11 +68,25 @@ struct AspArgs {
   int32_t n_ev;
   float mu;
   float lam;
+  PeerSync sync;
+};
+
+// scatter (fused path): copy every source's owner slices into the owners' inbox slots with posted NVLink stores:
+// for each source k and each rank q != rank: src[k][real_lo[q] .. real_hi[q]) -> inbox[q] + slot[k]*reg_len.
+struct ScatterArgs {
+  const float *src[kMaxWorkers];
+  int32_t slot[kMaxWorkers];
+  float *inbox[kMaxPeers];
+  int64_t reg_len;     // padded owner region (floats, multiple of 32): the slot stride and region size
+  int64_t P;
+  int32_t n_src;
+  PeerSync sync;
 };
 
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s);
+cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
                               cudaStream_t s);
 cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,

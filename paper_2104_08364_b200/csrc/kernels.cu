@@ -22,8 +22,66 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ float4 ld4(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+// Streaming 128-bit accesses: loads cached in L2 only (.cg — never a stale L1 line for data written by peers),
+// stores marked evict-first (.cs).
+__device__ __forceinline__ float4 ld4(const float *p) { return __ldcg(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ void st4(float *p, float4 x) { __stcs(reinterpret_cast<float4 *>(p), x); }
+
+// ---------------------------------------------------------------------------------------------------------------
+// Cross-GPU flag barrier (fused path). Release/acquire at system scope over NVLink-mapped peer memory; every wait
+// is bounded (kTimeoutNs) so a missing peer can never hang the GPU: the wait gives up and raises *err.
+constexpr unsigned long long kTimeoutNs = 10ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Block-wide: returns when every rank has signalled >= epoch (or on timeout).
+__device__ void peer_wait(const PeerSync &s, uint32_t epoch) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    bool timed_out = false;
+    for (int q = 0; q < s.world && !timed_out; ++q) {
+      while ((int32_t)(ld_acquire_sys(s.sig_local + q) - epoch) < 0) {
+        if (globaltimer() - t0 > kTimeoutNs) {
+          atomicExch(s.err, 1);
+          timed_out = true;
+          break;
+        }
+        __nanosleep(100);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Block-wide, at kernel end: the last CTA of the grid publishes signal_epoch to every rank (after a system-scope fence
+// that orders all of this grid's stores, local and remote, before the flag) and optionally waits for all ranks.
+__device__ void peer_done(const PeerSync &s) {
+  if (s.signal_epoch == 0) return;
+  __threadfence_system();
+  __syncthreads();
+  __shared__ uint32_t last;
+  if (threadIdx.x == 0) last = atomicAdd(s.ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) {
+    *s.ctr = 0;
+    __threadfence_system();
+    for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, s.signal_epoch);
+  }
+  if (s.end_wait) peer_wait(s, s.signal_epoch);
+}
 
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
@@ -56,6 +114,7 @@ constexpr int kG1 = 8;  // gradients loaded together
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
+  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
   const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -100,6 +159,8 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
         const int64_t q = q0 + u * stride;
         st4(a.w + 4 * q, wv[u]);
         st4(a.v + 4 * q, vv[u]);
+        for (int b = 0; b < a.n_bcast; ++b)   // fused path: the updated slice goes straight to every replica
+          *reinterpret_cast<float4 *>(a.bcast[b] + 4 * q) = wv[u];
       }
     }
     // scalar tail (count % 4 elements)
@@ -112,6 +173,7 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       bad |= nonfinite(w) | nonfinite(v);
       a.w[i] = w;
       a.v[i] = v;
+      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
     }
   } else {
     for (int64_t i = tid; i < a.count; i += stride) {
@@ -122,9 +184,11 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       bad |= nonfinite(w) | nonfinite(v);
       a.w[i] = w;
       a.v[i] = v;
+      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+  peer_done(a.sync);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -182,6 +246,7 @@ constexpr int kU2 = 4;
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_constant__ AspArgs a) {
+  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const float mu = a.mu, lam = a.lam;
@@ -274,6 +339,45 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+  peer_done(a.sync);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// scatter (fused path): every hosted gradient's owner slices go to the owners' inboxes with
+// posted 128-bit NVLink stores (the local slice is read in place by the owner update, never copied).
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int me = a.sync.rank;
+  const int64_t n4 = a.P >> 2, reg4 = a.reg_len >> 2;
+  constexpr int U = 4;
+  for (int k = 0; k < a.n_src; ++k) {
+    const float *src = a.src[k];
+    const int64_t slot_off = (int64_t)a.slot[k] * a.reg_len;
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * stride;
+        if (q < n4 && q / reg4 != me) x[u] = ld4(src + 4 * q);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * stride;
+        if (q < n4) {
+          const int64_t r = q / reg4;
+          if (r != me)
+            *reinterpret_cast<float4 *>(a.inbox[r] + slot_off + 4 * (q - r * reg4)) = x[u];
+        }
+      }
+    }
+    const int64_t i = 4 * n4 + tid;  // scalar tail
+    if (i < a.P) {
+      const int64_t r = i / a.reg_len;
+      if (r != me) a.inbox[r][slot_off + (i - r * a.reg_len)] = src[i];
+    }
+  }
+  peer_done(a.sync);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -392,10 +496,9 @@ int num_sms() {
 // grid-stride kernel (B200: 148 SMs).
 template <typename K>
 int grid_for(K kernel, int64_t work_items) {
-  static thread_local int resident = 0;
   int r = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
-  resident = r > 0 ? r : 1;
+  const int resident = r > 0 ? r : 1;
   int64_t want = (work_items + kThreads - 1) / kThreads;
   int64_t cap = (int64_t)resident * num_sms();
   if (want < 1) want = 1;
@@ -405,7 +508,7 @@ int grid_for(K kernel, int64_t work_items) {
 }  // namespace
 
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
-  if (a.count <= 0) return cudaSuccess;
+  if (a.count <= 0 && a.sync.wait_epoch == 0 && a.sync.signal_epoch == 0) return cudaSuccess;
   if (vec) {
     auto k = bsp_update_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
@@ -429,7 +532,7 @@ cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
 }
 
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
-  if (a.count <= 0 || a.n_ev <= 0) return cudaSuccess;
+  if ((a.count <= 0 || a.n_ev <= 0) && a.sync.wait_epoch == 0 && a.sync.signal_epoch == 0) return cudaSuccess;
   if (vec) {
     auto k = asp_replay_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);
@@ -437,6 +540,13 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     auto k = asp_replay_kernel<false>;
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s) {
+  auto k = scatter_kernel;
+  const int64_t work = a.n_src > 0 ? (a.P / 4 + 3) / 4 + 1 : 1;
+  k<<<grid_for(k, work), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -86,10 +86,22 @@ struct ss_ctx {
   // window batcher
   std::vector<Ev> win;
   int32_t max_win = 16;
+  // fused peer-memory path (G > 1): CUDA-IPC-mapped inboxes, replicas, pull buffers and flags
+  int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed
+  bool ipc_ready = false;
+  int64_t inbox_slots = 0;
+  float *inbox = nullptr;              // [inbox_slots][reg_len] gradient slices owned here, written by peers
+  float *pbuf = nullptr;               // [n_hosted][P_pad] pull buffers of hosted workers, written by owners
+  uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag
+  float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
+  uint32_t *peer_sig[ss::kMaxPeers] = {};
+  std::vector<void *> opened;          // peer mappings to close
+  uint32_t epoch = 0;
+  int32_t first_hosted = 0, n_hosted = 0;
   // instrumentation
   bool prof = false;
   std::vector<Timed> timed;
-  KStat kstat[3];
+  KStat kstat[4];
   std::string err;
 };
 
@@ -232,13 +244,181 @@ ss_status ensure_dist_buffers(ss_ctx *c) {
 }
 
 // ---------------------------------------------------------------------------------------------------------------
+// Fused peer-memory path setup (collective): allocate the inbox / pull buffers / flag block, exchange CUDA IPC
+// handles with one NCCL all-gather, map every peer's buffers. Re-run when more inbox slots are needed.
+void close_ipc(ss_ctx *c) {
+  for (void *p : c->opened) cudaIpcCloseMemHandle(p);
+  c->opened.clear();
+  cudaFree(c->inbox);
+  cudaFree(c->pbuf);
+  cudaFree(c->sigblk);
+  c->inbox = c->pbuf = nullptr;
+  c->sigblk = nullptr;
+  c->ipc_ready = false;
+}
+
+ss_status ensure_fused(ss_ctx *c, int64_t slots) {
+  if (c->ipc_ready && c->inbox_slots >= slots) return SS_OK;
+  if (c->world > ss::kMaxPeers) return fail(c, SS_E_INVAL, "fused path supports at most %d ranks", ss::kMaxPeers);
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  close_ipc(c);
+  slots = std::max<int64_t>(slots, std::max<int64_t>(c->n, c->max_win));
+  SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
+  SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+  SS_CUDA(c, cudaMalloc(&c->sigblk, 256 * sizeof(uint32_t)));
+  SS_CUDA(c, cudaMemset(c->sigblk, 0, 256 * sizeof(uint32_t)));
+  c->inbox_slots = slots;
+  c->epoch = 0;
+  cudaIpcMemHandle_t mine[4];
+  SS_CUDA(c, cudaIpcGetMemHandle(&mine[0], c->w));
+  SS_CUDA(c, cudaIpcGetMemHandle(&mine[1], c->inbox));
+  SS_CUDA(c, cudaIpcGetMemHandle(&mine[2], c->pbuf));
+  SS_CUDA(c, cudaIpcGetMemHandle(&mine[3], c->sigblk));
+  char *dev = nullptr;
+  const size_t per = sizeof mine;
+  SS_CUDA(c, cudaMalloc(&dev, per * c->world));
+  SS_CUDA(c, cudaMemcpy(dev + per * c->rank, mine, per, cudaMemcpyHostToDevice));
+  SS_NCCL(c, ncclAllGather(dev + per * c->rank, dev, per, ncclChar, c->comm, c->stream));
+  std::vector<cudaIpcMemHandle_t> all(4 * c->world);
+  SS_CUDA(c, cudaMemcpyAsync(all.data(), dev, per * c->world, cudaMemcpyDeviceToHost, c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(dev);
+  for (int32_t q = 0; q < c->world; ++q) {
+    if (q == c->rank) {
+      c->peer_w[q] = c->w;
+      c->peer_inbox[q] = c->inbox;
+      c->peer_pbuf[q] = c->pbuf;
+      c->peer_sig[q] = c->sigblk;
+      continue;
+    }
+    void *p[4];
+    for (int k = 0; k < 4; ++k) {
+      SS_CUDA(c, cudaIpcOpenMemHandle(&p[k], all[4 * q + k], cudaIpcMemLazyEnablePeerAccess));
+      c->opened.push_back(p[k]);
+    }
+    c->peer_w[q] = (float *)p[0];
+    c->peer_inbox[q] = (float *)p[1];
+    c->peer_pbuf[q] = (float *)p[2];
+    c->peer_sig[q] = (uint32_t *)p[3];
+  }
+  // every rank has mapped every peer before anyone signals through the mappings
+  SS_NCCL(c, ncclAllGather(c->sigblk + 128 + c->rank, c->sigblk + 128, 1, ncclUint32, c->comm, c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->ipc_ready = true;
+  return SS_OK;
+}
+
+ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bool end_wait) {
+  ss::PeerSync p;
+  std::memset(&p, 0, sizeof p);
+  p.sig_local = c->sigblk;
+  for (int32_t q = 0; q < c->world; ++q) p.sig_peer[q] = c->peer_sig[q];
+  p.ctr = c->sigblk + 32;
+  p.err = reinterpret_cast<int *>(c->sigblk + 64);
+  p.rank = c->rank;
+  p.world = c->world;
+  p.wait_epoch = wait_epoch;
+  p.signal_epoch = signal_epoch;
+  p.end_wait = end_wait ? 1 : 0;
+  return p;
+}
+
+// Phase A of every fused exchange: hosted sources' owner slices -> owners' inbox slots, then signal `epoch`.
+ss_status launch_scatter(ss_ctx *c, const std::vector<std::pair<const float *, int32_t>> &src, uint32_t epoch) {
+  ss::ScatterArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n_src = (int32_t)src.size();
+  for (size_t k = 0; k < src.size(); ++k) {
+    a.src[k] = src[k].first;
+    a.slot[k] = src[k].second;
+    if (!aligned16(src[k].first)) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
+  }
+  for (int32_t q = 0; q < c->world; ++q) a.inbox[q] = c->peer_inbox[q];
+  a.reg_len = c->reg_len;
+  a.P = c->P;
+  a.sync = peer_sync(c, 0, epoch, false);
+  Timed t;
+  timed_begin(c, &t, 3, 8.0 * (double)c->P * (double)src.size() * (c->world - 1) / c->world);
+  SS_CUDA(c, ss::launch_scatter(a, c->stream));
+  timed_end(c, &t);
+  return SS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
 // ASP window flush: [G>1: grouped send/recv of gradient shards to owners] -> asp_replay on the owned slice ->
 // [G>1: grouped send/recv of snapshot shards to pullers] -> D2H of host destinations.
+int32_t first_hosted_of(const ss_ctx *c, int32_t rank) {
+  int32_t j = 0;
+  while (j < c->n && host_of(c, j) < rank) ++j;
+  return j;
+}
+
+// Fused ASP window (G > 1): scatter the hosted pushes' owner slices (phase A), then every owner replays the window on
+// its slice and stores each pull's snapshot slice straight into the puller's mapped pull buffer (phase B); hosted
+// pulls are then copied from the pull buffer to the caller's destination.
+ss_status flush_fused(ss_ctx *c) {
+  SS_TRY(ensure_fused(c, c->max_win));
+  const int32_t me = c->rank;
+  const int64_t lo = c->real_lo[me], cnt = c->real_hi[me] - lo;
+  const uint32_t epA = ++c->epoch, epB = ++c->epoch;
+  std::vector<std::pair<const float *, int32_t>> src;
+  for (size_t k = 0; k < c->win.size(); ++k) {
+    const Ev &e = c->win[k];
+    if (e.kind == 0 && host_of(c, e.worker) == me) src.push_back({e.src, (int32_t)k});
+  }
+  SS_TRY(launch_scatter(c, src, epA));
+  ss::AspArgs a;
+  std::memset(&a, 0, sizeof a);
+  bool vec = true;
+  int32_t ne = 0, n_push = 0, n_pull = 0;
+  for (size_t k = 0; k < c->win.size(); ++k) {
+    const Ev &e = c->win[k];
+    ss::AspEvent &x = a.ev[ne];
+    x.kind = e.kind;
+    if (e.kind == 0) {
+      x.src = host_of(c, e.worker) == me ? e.src + lo : c->inbox + (int64_t)k * c->reg_len;
+      x.lr = e.lr;
+      vec = vec && aligned16(x.src);
+      ++n_push;
+    } else {
+      if (!e.data) continue;
+      const int32_t h = host_of(c, e.worker);
+      x.dst = c->peer_pbuf[h] + (int64_t)(e.worker - first_hosted_of(c, h)) * c->P_pad + lo;
+      ++n_pull;
+    }
+    ++ne;
+  }
+  a.n_ev = ne;
+  a.w = c->w + lo;
+  a.v = c->v;
+  a.flag = c->flag;
+  a.count = cnt;
+  a.mu = c->mu;
+  a.lam = c->lam;
+  a.sync = peer_sync(c, epA, epB, true);
+  Timed t;
+  timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
+  SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
+  timed_end(c, &t);
+  for (const Ev &e : c->win) {
+    if (e.kind != 1 || !e.data || host_of(c, e.worker) != me) continue;
+    const float *pb = c->pbuf + (int64_t)(e.worker - c->first_hosted) * c->P_pad;
+    if (e.host_dst)
+      SS_CUDA(c, cudaMemcpyAsync(e.host_dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    else
+      SS_CUDA(c, cudaMemcpyAsync(e.dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  c->win.clear();
+  c->stage_used = 0;
+  return SS_OK;
+}
+
 ss_status flush(ss_ctx *c) {
   if (c->win.empty()) {
     c->stage_used = 0;
     return SS_OK;
   }
+  if (c->world > 1 && c->fused_mode != 0) return flush_fused(c);
   const int32_t me = c->rank;
   const int64_t lo = c->real_lo[me], hi = c->real_hi[me], cnt = hi - lo;
   int32_t n_push = 0, n_pull = 0;
@@ -355,6 +535,14 @@ ss_status check_live(ss_ctx *c) {
 }
 
 ss_status enqueue(ss_ctx *c, const Ev &e) {
+  if (c->world > 1 && c->fused_mode != 0 && e.kind == 1) {
+    // fused windows hold one pull per worker (one mapped pull buffer per hosted worker)
+    for (const Ev &x : c->win)
+      if (x.kind == 1 && x.worker == e.worker) {
+        SS_TRY(flush(c));
+        break;
+      }
+  }
   c->win.push_back(e);
   if ((int32_t)c->win.size() >= c->max_win) return flush(c);
   return SS_OK;
@@ -366,6 +554,11 @@ ss_status sync_impl(ss_ctx *c) {
   int h = 0;
   SS_CUDA(c, cudaMemcpy(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) c->diverged = true;
+  if (c->ipc_ready) {
+    int t = 0;
+    SS_CUDA(c, cudaMemcpy(&t, c->sigblk + 64, sizeof(int), cudaMemcpyDeviceToHost));
+    if (t) return fail(c, SS_E_CUDA, "fused path: a cross-GPU barrier timed out (a peer did not arrive)");
+  }
   if (c->diverged) return fail(c, SS_E_DIVERGED, "diverged: a non-finite parameter or momentum was produced");
   return SS_OK;
 }
@@ -442,6 +635,9 @@ ss_status ss_init_dist(ss_ctx *c, int32_t rank, int32_t world, const void *uid) 
     c->real_lo[r] = std::min<int64_t>((int64_t)r * c->reg_len, c->P);
     c->real_hi[r] = std::min<int64_t>((int64_t)(r + 1) * c->reg_len, c->P);
   }
+  c->first_hosted = first_hosted_of(c, rank);
+  c->n_hosted = 0;
+  for (int32_t j = 0; j < c->n; ++j) c->n_hosted += host_of(c, j) == rank;
   // momentum now covers the owned region only
   float *v = nullptr;
   SS_CUDA(c, cudaMalloc(&v, (size_t)c->reg_len * sizeof(float)));
@@ -462,6 +658,7 @@ void ss_destroy(ss_ctx *c) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
+  close_ipc(c);
   if (c->comm) ncclCommDestroy(c->comm);
   for (float *p : c->stage) cudaFree(p);
   for (float *p : c->rslot) cudaFree(p);
@@ -551,6 +748,61 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     a.count = c->P;
     Timed t;
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
+    SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
+    timed_end(c, &t);
+  } else if (c->fused_mode != 0) {
+    // Fused peer-memory BSP. Phase A: scatter hosted gradients (exact mode) or this rank's
+    // pre-sum (mode 2) into the owners' inboxes. Phase B: owner sums its inbox slots in ascending order, updates
+    // w and v, and stores the new w slice into every rank's replica; one flag barrier closes the step.
+    const bool presum = c->fused_mode == 2;
+    SS_TRY(ensure_fused(c, presum ? c->world : c->n));
+    SS_TRY(ensure_dist_buffers(c));
+    const uint32_t epA = ++c->epoch, epB = ++c->epoch;
+    const int32_t me = c->rank;
+    const int64_t lo = c->real_lo[me], cnt = c->real_hi[me] - lo;
+    std::vector<std::pair<const float *, int32_t>> src;
+    if (presum) {
+      if (k > 0) {
+        ss::SumArgs sa;
+        std::memset(&sa, 0, sizeof sa);
+        for (int32_t i = 0; i < k; ++i) sa.g[i] = a.g[i];
+        sa.n_in = k;
+        sa.out = c->sum_buf;
+        sa.count = c->P;
+        sa.count_pad = c->P_pad;
+        Timed t;
+        timed_begin(c, &t, 2, 4.0 * ((double)c->P * k + (double)c->P_pad));
+        SS_CUDA(c, ss::launch_local_sum(sa, vec, c->stream));
+        timed_end(c, &t);
+      } else {
+        SS_CUDA(c, cudaMemsetAsync(c->sum_buf, 0, (size_t)c->P_pad * sizeof(float), c->stream));
+      }
+      src.push_back({c->sum_buf, me});
+    } else {
+      for (int32_t i = 0; i < k; ++i) src.push_back({a.g[i], c->first_hosted + i});
+    }
+    SS_TRY(launch_scatter(c, src, epA));
+    const float *hosted_g[ss::kMaxWorkers];
+    for (int32_t i = 0; i < k; ++i) hosted_g[i] = a.g[i];
+    std::memset(a.g, 0, sizeof a.g);
+    if (presum) {
+      for (int32_t q = 0; q < c->world; ++q)
+        a.g[q] = q == me ? c->sum_buf + lo : c->inbox + (int64_t)q * c->reg_len;
+      a.n_in = c->world;
+    } else {
+      for (int32_t j = 0; j < c->n; ++j)
+        a.g[j] = host_of(c, j) == me ? hosted_g[j - c->first_hosted] + lo : c->inbox + (int64_t)j * c->reg_len;
+      a.n_in = c->n;
+    }
+    a.w = c->w + lo;
+    a.v = c->v;
+    a.count = cnt;
+    a.n_bcast = 0;
+    for (int32_t q = 0; q < c->world; ++q)
+      if (q != me) a.bcast[a.n_bcast++] = c->peer_w[q] + lo;
+    a.sync = peer_sync(c, epA, epB, true);
+    Timed t;
+    timed_begin(c, &t, 0, 4.0 * (double)cnt * (a.n_in + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
   } else {
@@ -735,6 +987,14 @@ ss_status ss_set_window(ss_ctx *c, int32_t max_events) {
   return SS_OK;
 }
 
+ss_status ss_set_fused(ss_ctx *c, int32_t mode) {
+  SS_TRY(check_live(c));
+  if (mode < 0 || mode > 2) return fail(c, SS_E_INVAL, "fused mode must be 0, 1 or 2");
+  SS_TRY(flush(c));
+  c->fused_mode = mode;
+  return SS_OK;
+}
+
 ss_status ss_get_stream(ss_ctx *c, void **s) {
   if (!c || !s) return SS_E_INVAL;
   *s = c->stream;
@@ -761,7 +1021,7 @@ ss_status ss_profile(ss_ctx *c, int32_t on) {
 }
 
 ss_status ss_kernel_stats(ss_ctx *c, int32_t id, int64_t *launches, double *ms, double *bytes) {
-  if (!c || id < 0 || id > 2) return SS_E_INVAL;
+  if (!c || id < 0 || id > 3) return SS_E_INVAL;
   SS_TRY(drain_timed(c));
   if (launches) *launches = c->kstat[id].launches;
   if (ms) *ms = c->kstat[id].ms;

@@ -25,7 +25,7 @@ STATUS = ["SS_OK", "SS_E_INVAL", "SS_E_STATE", "SS_E_PROTOCOL", "SS_E_BARRIER", 
  SS_E_OOM) = range(10)
 
 # every symbol include/syncswitch.h declares (tests check the library exports each one)
-EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_last_error", "ss_set_lr_schedule",
+EXPORTS = ["ss_init", "ss_init_dist", "ss_set_fused", "ss_nccl_unique_id", "ss_destroy", "ss_last_error", "ss_set_lr_schedule",
            "ss_set_lr_policy", "ss_current_lr", "ss_bsp_step", "ss_asp_push", "ss_pull", "ss_switch",
            "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
@@ -54,6 +54,7 @@ def _load():
     sig = {
         "ss_init": [p, p, i64, i32, i32, f32, f32],
         "ss_init_dist": [p, i32, i32, p],
+        "ss_set_fused": [p, i32],
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
         "ss_set_lr_policy": [p, i32, f32],
@@ -346,6 +347,9 @@ class SyncSwitch:
 
     def init_dist(self, rank: int, world: int, uid: bytes):
         return self._chk(ss_init_dist(self.ctx, rank, world, uid))
+
+    def set_fused(self, mode: int):
+        return self._chk(lib.ss_set_fused(self.ctx, mode))
 
     def set_lr_schedule(self, boundaries, factors):
         return self._chk(ss_set_lr_schedule(self.ctx, boundaries, factors))

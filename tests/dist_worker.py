@@ -1,0 +1,100 @@
+"""One rank of the multi-GPU parity run (launched by tests/test_multi_gpu.py through torchrun, one process per GPU).
+
+Runs, through the C-ABI at G ranks: BSP supersteps, an in-place switch, a seeded ASP schedule with pulls, a switch
+back and more BSP steps, on synth_grad gradients. Writes the protocol integers, the final parameters and momentum,
+and every pull snapshot of the workers hosted here to <out>/rank<r>.npz. The test compares them with the oracle.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2104_08364_b200 import syncswitch as ss  # noqa: E402
+
+SEED = 20241018
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--P", type=int, default=100003)
+    ap.add_argument("--nworkers", type=int, default=4)
+    ap.add_argument("--nshards", type=int, default=4)
+    ap.add_argument("--window", type=int, default=7)
+    ap.add_argument("--bsp1", type=int, default=3)
+    ap.add_argument("--pushes", type=int, default=60)
+    ap.add_argument("--bsp2", type=int, default=2)
+    ap.add_argument("--fused", type=int, default=-1)
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P, n, S = a.P, a.nworkers, a.nshards
+    hosted = [j for j in range(n) if (j * world) // n == rank]
+
+    w0 = torch.empty(P, device="cuda")
+    ss.ss_check(ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0))
+    w0.mul_(64.0)
+    torch.cuda.synchronize()
+    g = ss.SyncSwitch(w0, S, n, 0.1, 0.9)
+    uid = [ss.ss_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    g.init_dist(rank, world, uid[0])
+    if a.fused >= 0:
+        g.set_fused(a.fused)
+    g.set_window(a.window)
+    g.set_lr_schedule([a.bsp1 + 10], [0.5])
+    counter = {j: 0 for j in range(n)}
+    keep = []
+
+    def grad(j):
+        k = counter[j]
+        counter[j] += 1
+        if j not in hosted:
+            return None
+        buf = torch.empty(P, device="cuda")
+        ss.ss_check(ss.ss_synth_grad(SEED, j, k, 0, P, buf))
+        keep.append(buf)
+        return buf
+
+    for _ in range(a.bsp1):
+        gs = {j: grad(j) for j in range(n)}
+        g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
+    g.switch(ss.SS_ASP, 0)
+    kind, worker, _ = ss.ss_schedule(n, [1000 + 100 * j for j in range(n)], a.pushes, jitter=100, seed=7)[1]
+    base, stale, snaps = {}, [], []
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            dst = torch.empty(P, device="cuda") if j in hosted else None
+            base[j] = g.pull(j, dst)
+            if dst is not None:
+                snaps.append(dst)
+        else:
+            stale.append(g.asp_push(j, grad(j), base[j]))
+    g.switch(ss.SS_BSP, 0)
+    for _ in range(a.bsp2):
+        gs = {j: grad(j) for j in range(n)}
+        g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
+    g.sync()
+    w = g.params()
+    v = g.velocity()
+    st = g.stats(64)
+    np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=w, v=v, stale=np.array(stale), log=g.log(),
+             hist=st["hist"], version=st["version"], dropped=st["dropped"],
+             snaps=np.stack([s.cpu().numpy() for s in snaps]) if snaps else np.zeros((0, P), np.float32),
+             hosted=np.array(hosted))
+    g.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,105 @@
+"""Multi-GPU parity (G = 2 and 4 ranks, one process per GPU via torchrun, NCCL over NVLink) against the oracle.
+
+Pure-ASP runs are bit-exact at any G (owner routing moves data, the arithmetic per element is unchanged). Runs with
+NCCL BSP supersteps match within the C13 tolerance (NCCL's reduce-scatter summation order differs from ascending
+workers) unless the fused peer-memory path (bit-exact, ascending workers) is selected. Protocol
+integers are exact in every case. Skipped when the box has fewer GPUs than ranks.
+"""
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SEED = 20241018
+
+
+def oracle_run(orc, P, n, S, bsp1, pushes, bsp2):
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    o.set_lr_schedule([bsp1 + 10], [0.5])
+    counter = {j: 0 for j in range(n)}
+
+    def grad(j):
+        k = counter[j]
+        counter[j] += 1
+        return orc.synth_grad(SEED, j, k, 0, P)
+
+    for _ in range(bsp1):
+        assert o.bsp_step([grad(j) for j in range(n)]) == 0
+    o.switch(orc.ASP, 0)
+    kind, worker, _ = orc.schedule(n, [1000 + 100 * j for j in range(n)], pushes, jitter=100, seed=7)
+    base, stale, snaps = {}, [], {j: [] for j in range(n)}
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            _, s, base[j] = o.pull(j)
+            snaps[j].append(s)
+        else:
+            rc, st = o.asp_push(j, grad(j), base[j])
+            assert rc == 0
+            stale.append(st)
+    o.switch(orc.BSP, 0)
+    for _ in range(bsp2):
+        assert o.bsp_step([grad(j) for j in range(n)]) == 0
+    return o, stale, snaps, kind, worker
+
+
+def launch(world, args, tmp):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}",
+           os.path.join(ROOT, "tests", "dist_worker.py"), "--out", tmp, *map(str, args)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def close_c13(x, y, rel=1e-5):
+    x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+    rms = np.sqrt(np.mean(y * y))
+    return bool(np.all(np.abs(x - y) <= rel * np.abs(y) + rel * rms))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", ["asp_only", "switched", "switched_fused"])
+def test_multi_gpu_parity(orc, world, case):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S, win = 100003, 8, 8, 7
+    bsp1, pushes, bsp2 = (0, 80, 0) if case == "asp_only" else (3, 60, 2)
+    fused = 1 if case == "switched_fused" else 0
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", win, "--bsp1", bsp1, "--pushes", pushes,
+                       "--bsp2", bsp2, "--fused", fused], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2)
+    exact = case != "switched"
+    ow, ov = o.params(), o.velocity()
+    for r in res:
+        # protocol integers: exact on every rank
+        assert list(r["stale"]) == stale
+        assert np.array_equal(r["log"], o.log())
+        assert int(r["version"]) == o.version and np.array_equal(r["hist"], o.stats(64)["hist"])
+        if exact:
+            assert np.array_equal(r["w"], ow) and np.array_equal(r["v"], ov)
+        else:
+            assert close_c13(r["w"], ow) and close_c13(r["v"], ov)
+        hosted = [int(j) for j in r["hosted"]]
+        want = [s for kd, j in zip(kind, worker) if kd == 1 and int(j) in hosted
+                for s in [None]]
+        # snapshots of hosted workers in event order
+        exp = []
+        cnt = {j: 0 for j in hosted}
+        for kd, j in zip(kind, worker):
+            j = int(j)
+            if kd == 1 and j in hosted:
+                exp.append(snaps[j][cnt[j]])
+                cnt[j] += 1
+        assert len(exp) == len(r["snaps"]) == len(want)
+        for a, b in zip(r["snaps"], exp):
+            assert np.array_equal(a, b) if exact else close_c13(a, b)
