@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fused", default="auto", choices=["auto", "0", "1", "2"],
+                    help="G>1 exchange: 0 NCCL, 1 fused exact, 2 fused pre-summed; auto = 1 if n <= G else 2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -147,6 +149,9 @@ def run_ours(args):
         uid = [ss.ss_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         g.init_dist(rank, world, uid[0])
+    fused = (1 if n <= world else 2) if args.fused == "auto" else int(args.fused)
+    if world > 1:
+        g.set_fused(fused)
     g.set_window(win)
     del w0
 
@@ -154,7 +159,10 @@ def run_ours(args):
     ring = {(j, r): torch.empty(P, device="cuda") for j in hosted for r in range(2)}
     for (j, r), buf in ring.items():
         ss.ss_check(ss.ss_synth_grad(SEED, j, r, 0, P, buf))
-    pull_dst = {j: torch.empty(P, device="cuda") for j in hosted}
+    if world > 1 and fused:
+        pull_dst = {j: g.pull_buffer(j) for j in hosted}     # zero-copy pulls into the NVLink-mapped buffers
+    else:
+        pull_dst = {j: torch.empty(P, device="cuda") for j in hosted}
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(g.stream)
 
@@ -275,6 +283,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash gradients)",
         "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "asp_window_events": win,
                    "parallelism": f"sharded PS over {world} GPU(s)",
+                   "exchange": "single GPU" if world == 1 else
+                   ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed"][fused],
                    "l2": "inputs larger than L2 (~3.3 GB streamed per step vs 126 MB L2), no flush"},
         "phases": phases, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
         "e2e": e2e,

@@ -88,6 +88,12 @@ ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *ncc
  * Errors: SS_E_INVAL. */
 ss_status ss_set_fused(ss_ctx *ctx, int32_t mode);
 
+/* Fused multi-GPU mode: the CUDA-IPC-mapped pull buffer (device fp32[P_pad], owned by the context, valid until
+ * ss_destroy) of a worker hosted on this rank. Owners store each pull's snapshot slices into it over NVLink; passing
+ * it as ss_pull's dst makes the pull zero-copy (otherwise the snapshot is copied from it into dst). Collective on
+ * first use. Errors: SS_E_INVAL (worker not hosted here), SS_E_STATE (single GPU or NCCL mode). */
+ss_status ss_pull_buffer(ss_ctx *ctx, int32_t worker, float **out);
+
 /* Fills the 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
 ss_status ss_nccl_unique_id(void *out128);
 
@@ -236,6 +242,20 @@ ss_status ss_detector_new(ss_detector **out, int32_t n, int32_t K);
 ss_status ss_detector_window(ss_detector *dt, const double *samples, const double *busy, int32_t *straggler,
                              int32_t *clean_out);
 void ss_detector_free(ss_detector *dt);
+
+/* Multi-GPU routing plan (SV §8(a) a8/a10, §8(e)) of an ASP event sequence as rank `rank` of `world` executes it:
+ * the sequence is cut into replay windows exactly as the runtime cuts them (max_window events; in fused mode also
+ * before a second pull of the same worker), and each window yields, in issue order, phase-0 ops (gradient slice of a
+ * push: hosting rank -> every other owner) and phase-1 ops (snapshot slice of a pull: every other owner -> hosting
+ * rank). op 0 = send (fused: posted NVLink store), 1 = recv. offset/count: the slice [offset, offset+count) of the
+ * full vector. Writes min(cap, total) ops; *n_ops = total, *n_windows = windows. Host only. Errors: SS_E_INVAL. */
+typedef struct {
+  int32_t window, phase, op, peer, event;
+  int64_t offset, count;
+} ss_route_op;
+ss_status ss_route_plan(int32_t rank, int32_t world, int32_t n_workers, int32_t n_shards, int64_t n_params,
+                        int32_t max_window, int32_t fused, const int32_t *kind, const int32_t *worker, int64_t n_ev,
+                        ss_route_op *ops, int64_t cap, int64_t *n_ops, int32_t *n_windows);
 
 /* Greedy online policy: given the detector's verdict, the protocol and the BSP quota, returns the switch
  * to issue now: -1 none, SS_ASP (a straggler appeared during BSP), SS_BSP (cluster clean, ASP, BSP quota unmet). */

@@ -14,7 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsyncswitch.so")
 SOURCES = ["runtime.cu", "kernels.cu", "control.cpp"]
-HEADERS = ["internal.h"]
+HEADERS_EXTRA = ["plan.h"]
+HEADERS = ["internal.h", "plan.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1,11 +1,82 @@
 // control.cpp — host control plane of the Sync-Switch path: Table I remap, seeded arrival schedule, straggler
 // detector and greedy policy. Host-only C++ (no CUDA); exported through include/syncswitch.h.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <new>
 #include <vector>
 
+#include "plan.h"
 #include "syncswitch.h"
+
+namespace ss {
+
+int32_t Layout::first_hosted(int32_t r) const {
+  int32_t j = 0;
+  while (j < n && host(j) < r) ++j;
+  return j;
+}
+
+int32_t Layout::n_hosted(int32_t r) const {
+  int32_t c = 0;
+  for (int32_t j = 0; j < n; ++j) c += host(j) == r;
+  return c;
+}
+
+Layout make_layout(int64_t P, int32_t S, int32_t n, int32_t rank, int32_t world) {
+  Layout L;
+  L.rank = rank;
+  L.world = world;
+  L.n = n;
+  L.S = S;
+  L.P = P;
+  L.pad = (((P + S - 1) / S) + 31) / 32 * 32;
+  L.P_pad = L.pad * S;
+  L.reg_len = L.P_pad / world;
+  L.real_lo.resize(world);
+  L.real_hi.resize(world);
+  for (int32_t r = 0; r < world; ++r) {
+    L.real_lo[r] = std::min<int64_t>((int64_t)r * L.reg_len, P);
+    L.real_hi[r] = std::min<int64_t>((int64_t)(r + 1) * L.reg_len, P);
+  }
+  return L;
+}
+
+void plan_window(const Layout &L, const int32_t *kind, const int32_t *worker, const uint8_t *data, int32_t n_ev,
+                 std::vector<RouteOp> &out) {
+  const int32_t me = L.rank;
+  for (int32_t k = 0; k < n_ev; ++k) {  // phase 0: every push's slices to their owners
+    if (kind[k] != 0) continue;
+    const int32_t h = L.host(worker[k]);
+    if (h == me) {
+      for (int32_t r = 0; r < L.world; ++r)
+        if (r != me && L.count(r) > 0) out.push_back({0, 0, r, k, L.real_lo[r], L.count(r)});
+    } else if (L.count(me) > 0) {
+      out.push_back({0, 1, h, k, L.real_lo[me], L.count(me)});
+    }
+  }
+  for (int32_t k = 0; k < n_ev; ++k) {  // phase 1: every pull's snapshot slices to the puller
+    if (kind[k] != 1 || !data[k]) continue;
+    const int32_t h = L.host(worker[k]);
+    if (h == me) {
+      for (int32_t r = 0; r < L.world; ++r)
+        if (r != me && L.count(r) > 0) out.push_back({1, 1, r, k, L.real_lo[r], L.count(r)});
+    } else if (L.count(me) > 0) {
+      out.push_back({1, 0, h, k, L.real_lo[me], L.count(me)});
+    }
+  }
+}
+
+bool window_cut(const int32_t *kind, const int32_t *worker, int32_t n_in_window, int32_t new_kind, int32_t new_worker,
+                int32_t max_window, bool fused) {
+  if (n_in_window >= max_window) return true;
+  if (fused && new_kind == 1)
+    for (int32_t k = 0; k < n_in_window; ++k)
+      if (kind[k] == 1 && worker[k] == new_worker) return true;
+  return false;
+}
+
+}  // namespace ss
 
 namespace {
 
@@ -131,6 +202,47 @@ ss_status ss_detector_window(ss_detector *d, const double *samples, const double
 }
 
 void ss_detector_free(ss_detector *d) { delete d; }
+
+// Routing plan of a whole ASP event sequence as seen by `rank` (window cuts + per-window ops), for CPU tests of the
+// multi-GPU host logic. Window k of the sequence is reported in ops[i].window; event indices are window-relative.
+ss_status ss_route_plan(int32_t rank, int32_t world, int32_t n_workers, int32_t n_shards, int64_t n_params,
+                        int32_t max_window, int32_t fused, const int32_t *kind, const int32_t *worker, int64_t n_ev,
+                        ss_route_op *ops, int64_t cap, int64_t *n_ops, int32_t *n_windows) {
+  if (world < 1 || rank < 0 || rank >= world || n_workers < 1 || n_shards < 1 || n_shards % world || n_params < 1 ||
+      max_window < 1 || max_window > 64 || n_ev < 0 || (n_ev > 0 && (!kind || !worker)) || !n_ops || cap < 0 ||
+      (cap > 0 && !ops))
+    return SS_E_INVAL;
+  const ss::Layout L = ss::make_layout(n_params, n_shards, n_workers, rank, world);
+  std::vector<int32_t> wk, ww;
+  std::vector<uint8_t> wd;
+  std::vector<ss::RouteOp> plan;
+  int64_t total = 0;
+  int32_t win_id = 0;
+  auto emit = [&]() {
+    if (wk.empty()) return;
+    plan.clear();
+    ss::plan_window(L, wk.data(), ww.data(), wd.data(), (int32_t)wk.size(), plan);
+    for (const ss::RouteOp &o : plan) {
+      if (total < cap) ops[total] = ss_route_op{win_id, o.phase, o.op, o.peer, o.event, o.offset, o.count};
+      ++total;
+    }
+    ++win_id;
+    wk.clear();
+    ww.clear();
+    wd.clear();
+  };
+  for (int64_t i = 0; i < n_ev; ++i) {
+    if (ss::window_cut(wk.data(), ww.data(), (int32_t)wk.size(), kind[i], worker[i], max_window, fused != 0)) emit();
+    wk.push_back(kind[i]);
+    ww.push_back(worker[i]);
+    wd.push_back(1);
+    if ((int32_t)wk.size() >= max_window) emit();
+  }
+  emit();
+  *n_ops = total;
+  if (n_windows) *n_windows = win_id;
+  return SS_OK;
+}
 
 // Greedy policy: "simply switches to ASP ... when a straggler is detected; once the cluster is free of any
 // stragglers and the aggregate BSP training has not been satisfied, it will switch back to training with BSP".

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "plan.h"
 #include "syncswitch.h"
 
 namespace {
@@ -59,6 +60,7 @@ struct ss_ctx {
   std::vector<float> factors;
   // distribution
   int32_t rank = 0, world = 1;
+  ss::Layout L;                        // shard layout / ownership (plan.h)
   ncclComm_t comm = nullptr;
   int64_t reg_len = 0;                 // padded owner region length (P_pad / world)
   std::vector<int64_t> real_lo, real_hi;  // per rank: real (unpadded) element range of its region
@@ -246,29 +248,35 @@ ss_status ensure_dist_buffers(ss_ctx *c) {
 // ---------------------------------------------------------------------------------------------------------------
 // Fused peer-memory path setup (collective): allocate the inbox / pull buffers / flag block, exchange CUDA IPC
 // handles with one NCCL all-gather, map every peer's buffers. Re-run when more inbox slots are needed.
-void close_ipc(ss_ctx *c) {
+// Unmaps the peers and frees the inbox; `all` also frees the pull buffers and the flag block (destroy only: they
+// keep their addresses — ss_pull_buffer hands them out — and the flags keep their epochs across re-setups).
+void close_ipc(ss_ctx *c, bool all) {
   for (void *p : c->opened) cudaIpcCloseMemHandle(p);
   c->opened.clear();
   cudaFree(c->inbox);
-  cudaFree(c->pbuf);
-  cudaFree(c->sigblk);
-  c->inbox = c->pbuf = nullptr;
-  c->sigblk = nullptr;
+  c->inbox = nullptr;
   c->ipc_ready = false;
+  if (all) {
+    cudaFree(c->pbuf);
+    cudaFree(c->sigblk);
+    c->pbuf = nullptr;
+    c->sigblk = nullptr;
+  }
 }
 
 ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   if (c->ipc_ready && c->inbox_slots >= slots) return SS_OK;
   if (c->world > ss::kMaxPeers) return fail(c, SS_E_INVAL, "fused path supports at most %d ranks", ss::kMaxPeers);
   SS_CUDA(c, cudaStreamSynchronize(c->stream));
-  close_ipc(c);
+  close_ipc(c, false);
   slots = std::max<int64_t>(slots, std::max<int64_t>(c->n, c->max_win));
   SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
-  SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
-  SS_CUDA(c, cudaMalloc(&c->sigblk, 256 * sizeof(uint32_t)));
-  SS_CUDA(c, cudaMemset(c->sigblk, 0, 256 * sizeof(uint32_t)));
+  if (!c->pbuf) SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+  if (!c->sigblk) {
+    SS_CUDA(c, cudaMalloc(&c->sigblk, 256 * sizeof(uint32_t)));
+    SS_CUDA(c, cudaMemset(c->sigblk, 0, 256 * sizeof(uint32_t)));
+  }
   c->inbox_slots = slots;
-  c->epoch = 0;
   cudaIpcMemHandle_t mine[4];
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[0], c->w));
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[1], c->inbox));
@@ -403,6 +411,7 @@ ss_status flush_fused(ss_ctx *c) {
   for (const Ev &e : c->win) {
     if (e.kind != 1 || !e.data || host_of(c, e.worker) != me) continue;
     const float *pb = c->pbuf + (int64_t)(e.worker - c->first_hosted) * c->P_pad;
+    if (e.dst == pb) continue;  // zero-copy pull into the mapped pull buffer (ss_pull_buffer)
     if (e.host_dst)
       SS_CUDA(c, cudaMemcpyAsync(e.host_dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     else
@@ -427,21 +436,25 @@ ss_status flush(ss_ctx *c) {
     else if (e.data) ++n_pull;
   }
 
+  // routing plan of this window (plan.h; the same code ss_route_plan exposes to the CPU tests)
+  std::vector<ss::RouteOp> plan;
   if (c->world > 1) {
+    std::vector<int32_t> kd, wk;
+    std::vector<uint8_t> dt;
+    for (const Ev &e : c->win) {
+      kd.push_back(e.kind);
+      wk.push_back(e.worker);
+      dt.push_back(e.data ? 1 : 0);
+    }
+    ss::plan_window(c->L, kd.data(), wk.data(), dt.data(), (int32_t)kd.size(), plan);
     SS_TRY(ensure_dist_buffers(c));
     SS_NCCL(c, ncclGroupStart());
-    for (size_t k = 0; k < c->win.size(); ++k) {
-      const Ev &e = c->win[k];
-      if (e.kind != 0) continue;
-      const int32_t h = host_of(c, e.worker);
-      if (h == me) {
-        for (int32_t r = 0; r < c->world; ++r) {
-          const int64_t rc = c->real_hi[r] - c->real_lo[r];
-          if (r != me && rc > 0) SS_NCCL(c, ncclSend(e.src + c->real_lo[r], rc, ncclFloat, r, c->comm, c->stream));
-        }
-      } else if (cnt > 0) {
-        SS_NCCL(c, ncclRecv(c->rslot[k], cnt, ncclFloat, h, c->comm, c->stream));
-      }
+    for (const ss::RouteOp &o : plan) {
+      if (o.phase != 0) continue;
+      if (o.op == 0)
+        SS_NCCL(c, ncclSend(c->win[o.event].src + o.offset, o.count, ncclFloat, o.peer, c->comm, c->stream));
+      else
+        SS_NCCL(c, ncclRecv(c->rslot[o.event], o.count, ncclFloat, o.peer, c->comm, c->stream));
     }
     SS_NCCL(c, ncclGroupEnd());
   }
@@ -488,18 +501,12 @@ ss_status flush(ss_ctx *c) {
 
   if (c->world > 1) {
     SS_NCCL(c, ncclGroupStart());
-    for (size_t k = 0; k < c->win.size(); ++k) {
-      const Ev &e = c->win[k];
-      if (e.kind != 1 || !e.data) continue;
-      const int32_t h = host_of(c, e.worker);
-      if (h == me) {
-        for (int32_t r = 0; r < c->world; ++r) {
-          const int64_t rc = c->real_hi[r] - c->real_lo[r];
-          if (r != me && rc > 0) SS_NCCL(c, ncclRecv(e.dst + c->real_lo[r], rc, ncclFloat, r, c->comm, c->stream));
-        }
-      } else if (cnt > 0) {
-        SS_NCCL(c, ncclSend(c->sslot[k], cnt, ncclFloat, h, c->comm, c->stream));
-      }
+    for (const ss::RouteOp &o : plan) {
+      if (o.phase != 1) continue;
+      if (o.op == 0)
+        SS_NCCL(c, ncclSend(c->sslot[o.event], o.count, ncclFloat, o.peer, c->comm, c->stream));
+      else
+        SS_NCCL(c, ncclRecv(c->win[o.event].dst + o.offset, o.count, ncclFloat, o.peer, c->comm, c->stream));
     }
     SS_NCCL(c, ncclGroupEnd());
   }
@@ -535,14 +542,14 @@ ss_status check_live(ss_ctx *c) {
 }
 
 ss_status enqueue(ss_ctx *c, const Ev &e) {
-  if (c->world > 1 && c->fused_mode != 0 && e.kind == 1) {
-    // fused windows hold one pull per worker (one mapped pull buffer per hosted worker)
-    for (const Ev &x : c->win)
-      if (x.kind == 1 && x.worker == e.worker) {
-        SS_TRY(flush(c));
-        break;
-      }
+  std::vector<int32_t> kd, wk;
+  for (const Ev &x : c->win) {
+    kd.push_back(x.kind);
+    wk.push_back(x.worker);
   }
+  if (ss::window_cut(kd.data(), wk.data(), (int32_t)kd.size(), e.kind, e.worker, c->max_win,
+                     c->world > 1 && c->fused_mode != 0))
+    SS_TRY(flush(c));
   c->win.push_back(e);
   if ((int32_t)c->win.size() >= c->max_win) return flush(c);
   return SS_OK;
@@ -587,9 +594,10 @@ ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n
   c->off.resize(n_shards + 1);
   for (int32_t s = 0; s <= n_shards; ++s) c->off[s] = std::min<int64_t>((int64_t)s * c->pad, n_params);
   c->base.assign(n_workers, 0);
-  c->reg_len = c->P_pad;
-  c->real_lo = {0};
-  c->real_hi = {n_params};
+  c->L = ss::make_layout(n_params, n_shards, n_workers, 0, 1);
+  c->reg_len = c->L.reg_len;
+  c->real_lo = c->L.real_lo;
+  c->real_hi = c->L.real_hi;
   auto bail = [&](ss_status s) {
     ss_destroy(c);
     return s;
@@ -628,16 +636,12 @@ ss_status ss_init_dist(ss_ctx *c, int32_t rank, int32_t world, const void *uid) 
   SS_NCCL(c, ncclCommInitRank(&c->comm, world, id, rank));
   c->rank = rank;
   c->world = world;
-  c->reg_len = c->P_pad / world;
-  c->real_lo.resize(world);
-  c->real_hi.resize(world);
-  for (int32_t r = 0; r < world; ++r) {
-    c->real_lo[r] = std::min<int64_t>((int64_t)r * c->reg_len, c->P);
-    c->real_hi[r] = std::min<int64_t>((int64_t)(r + 1) * c->reg_len, c->P);
-  }
-  c->first_hosted = first_hosted_of(c, rank);
-  c->n_hosted = 0;
-  for (int32_t j = 0; j < c->n; ++j) c->n_hosted += host_of(c, j) == rank;
+  c->L = ss::make_layout(c->P, c->S, c->n, rank, world);
+  c->reg_len = c->L.reg_len;
+  c->real_lo = c->L.real_lo;
+  c->real_hi = c->L.real_hi;
+  c->first_hosted = c->L.first_hosted(rank);
+  c->n_hosted = c->L.n_hosted(rank);
   // momentum now covers the owned region only
   float *v = nullptr;
   SS_CUDA(c, cudaMalloc(&v, (size_t)c->reg_len * sizeof(float)));
@@ -658,7 +662,7 @@ void ss_destroy(ss_ctx *c) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
-  close_ipc(c);
+  close_ipc(c, true);
   if (c->comm) ncclCommDestroy(c->comm);
   for (float *p : c->stage) cudaFree(p);
   for (float *p : c->rslot) cudaFree(p);
@@ -992,6 +996,16 @@ ss_status ss_set_fused(ss_ctx *c, int32_t mode) {
   if (mode < 0 || mode > 2) return fail(c, SS_E_INVAL, "fused mode must be 0, 1 or 2");
   SS_TRY(flush(c));
   c->fused_mode = mode;
+  return SS_OK;
+}
+
+ss_status ss_pull_buffer(ss_ctx *c, int32_t worker, float **out) {
+  SS_TRY(check_live(c));
+  if (!out || worker < 0 || worker >= c->n) return fail(c, SS_E_INVAL, "bad worker or null output");
+  if (c->world == 1 || c->fused_mode == 0) return fail(c, SS_E_STATE, "pull buffers exist in fused multi-GPU mode");
+  if (host_of(c, worker) != c->rank) return fail(c, SS_E_INVAL, "worker %d is not hosted on this rank", worker);
+  SS_TRY(ensure_fused(c, c->max_win));
+  *out = c->pbuf + (int64_t)(worker - c->first_hosted) * c->P_pad;
   return SS_OK;
 }
 

@@ -25,18 +25,24 @@ STATUS = ["SS_OK", "SS_E_INVAL", "SS_E_STATE", "SS_E_PROTOCOL", "SS_E_BARRIER", 
  SS_E_OOM) = range(10)
 
 # every symbol include/syncswitch.h declares (tests check the library exports each one)
-EXPORTS = ["ss_init", "ss_init_dist", "ss_set_fused", "ss_nccl_unique_id", "ss_destroy", "ss_last_error", "ss_set_lr_schedule",
+EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_last_error", "ss_set_lr_schedule",
            "ss_set_lr_policy", "ss_current_lr", "ss_bsp_step", "ss_asp_push", "ss_pull", "ss_switch",
            "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
-           "ss_detector_free", "ss_greedy_decision"]
+           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer"]
 
 
 class SSError(RuntimeError):
     def __init__(self, status: int, msg: str = ""):
         self.status = status
         super().__init__(f"{STATUS[status] if 0 <= status < len(STATUS) else status}: {msg}")
+
+
+class ss_route_op(ctypes.Structure):
+    _fields_ = [("window", ctypes.c_int32), ("phase", ctypes.c_int32), ("op", ctypes.c_int32),
+                ("peer", ctypes.c_int32), ("event", ctypes.c_int32), ("offset", ctypes.c_int64),
+                ("count", ctypes.c_int64)]
 
 
 class ss_event(ctypes.Structure):
@@ -55,6 +61,7 @@ def _load():
         "ss_init": [p, p, i64, i32, i32, f32, f32],
         "ss_init_dist": [p, i32, i32, p],
         "ss_set_fused": [p, i32],
+        "ss_pull_buffer": [p, i32, p],
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
         "ss_set_lr_policy": [p, i32, f32],
@@ -80,6 +87,7 @@ def _load():
         "ss_schedule": [i32, p, i64, u64, i32, i64, i64, i64, i64, p, p, p, p],
         "ss_detector_new": [p, i32, i32],
         "ss_detector_window": [p, p, p, p, p],
+        "ss_route_plan": [i32, i32, i32, i32, i64, i32, i32, p, p, i64, p, i64, p, p],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -288,6 +296,25 @@ def ss_schedule(n: int, period, n_push: int, jitter: int = 0, seed: int = 7, slo
     return s, (kind[:ne.value], worker[:ne.value], tick[:ne.value])
 
 
+def ss_route_plan(rank: int, world: int, n_workers: int, n_shards: int, n_params: int, max_window: int, fused: bool,
+                  kind, worker):
+    """Routing plan of an ASP event sequence as `rank` executes it: (status, [(window, phase, op, peer, event,
+    offset, count)], n_windows)."""
+    k = _a(kind, np.int32)
+    w = _a(worker, np.int32)
+    total, nwin = ctypes.c_int64(), ctypes.c_int32()
+    s = lib.ss_route_plan(rank, world, n_workers, n_shards, n_params, max_window, int(fused), k.ctypes.data,
+                          w.ctypes.data, k.size, None, 0, ctypes.byref(total), ctypes.byref(nwin))
+    if s != SS_OK:
+        return s, [], 0
+    arr = (ss_route_op * max(total.value, 1))()
+    s = lib.ss_route_plan(rank, world, n_workers, n_shards, n_params, max_window, int(fused), k.ctypes.data,
+                          w.ctypes.data, k.size, ctypes.cast(arr, ctypes.c_void_p), total.value, ctypes.byref(total),
+                          ctypes.byref(nwin))
+    ops = [(o.window, o.phase, o.op, o.peer, o.event, o.offset, o.count) for o in arr[:total.value]]
+    return s, ops, nwin.value
+
+
 class Detector:
     """ss_detector_* (P:1425)."""
 
@@ -350,6 +377,11 @@ class SyncSwitch:
 
     def set_fused(self, mode: int):
         return self._chk(lib.ss_set_fused(self.ctx, mode))
+
+    def pull_buffer(self, worker: int) -> int:
+        out = ctypes.c_void_p()
+        self._chk(lib.ss_pull_buffer(self.ctx, worker, ctypes.byref(out)))
+        return out.value
 
     def set_lr_schedule(self, boundaries, factors):
         return self._chk(ss_set_lr_schedule(self.ctx, boundaries, factors))
