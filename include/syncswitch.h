@@ -262,6 +262,43 @@ ss_status ss_route_plan(int32_t rank, int32_t world, int32_t n_workers, int32_t 
 int32_t ss_greedy_decision(int32_t protocol, int32_t any_straggler, int32_t cluster_clean, int64_t bsp_done,
                            int64_t bsp_quota);
 
+/* ============================================================================================================
+ * Online straggler scenario (SV config 4; P:1410-1425 greedy policy, P:1416 transient <= 100 s)
+ * ============================================================================================================
+ * A discrete-event run in integer ticks (DESIGN reading C23). BSP supersteps last max_j T_j(t) + d_{j,k} ticks (the
+ * barrier waits for the slowest worker; busy time excludes the wait); under ASP every worker pushes after T_j + d and
+ * pulls at once (reading C7). Every detection window of `window_ticks` feeds the detector (samples B per completed
+ * worker step, busy ticks) and the greedy policy: straggler under BSP -> switch to ASP now; cluster clean under ASP and
+ * BSP quota unmet -> switch to BSP now (in-flight pushes then arrive late and are dropped). BSP samples reaching
+ * W * quota_num / quota_den switch to ASP for good (timing policy); the run ends when W samples are processed.
+ * Worker j's k-th gradient is synth_grad(grad_seed, j, k, ...). */
+typedef struct {
+  int32_t n_workers;
+  int64_t batch;          /* B samples per worker step */
+  int64_t total_samples;  /* W */
+  int64_t quota_num, quota_den;
+  int64_t period;         /* T ticks */
+  int64_t jitter;         /* J */
+  uint64_t sched_seed, grad_seed;
+  int32_t slow_worker;    /* -1: none */
+  int64_t slow_factor, slow_t0, slow_t1;
+  int64_t window_ticks;   /* detection window D */
+  int32_t K;              /* consecutive windows */
+} ss_scenario;
+typedef struct {
+  int64_t tick, version;
+  int32_t to_protocol, reason; /* reason 0: BSP quota met (timing policy), 1: straggler (greedy), 2: clean (greedy) */
+} ss_switch_event;
+typedef struct {
+  int64_t bsp_steps, asp_pushes, dropped, end_tick, version, windows;
+  int32_t n_switches;
+} ss_scenario_result;
+/* ctx: a context with n_workers workers (its stream runs the kernels; collective when distributed), or NULL for a
+ * host-only dry run of the same event sequence (no data). log: cap entries (nullable). Errors: SS_E_INVAL, and every
+ * error of the protocol calls it issues. */
+ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scenario_result *out, ss_switch_event *log,
+                          int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

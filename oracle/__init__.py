@@ -302,3 +302,30 @@ class Detector:
         if getattr(self, "_h", None):
             self._L.orc_detector_free(self._h)
             self._h = None
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# online straggler scenario (config 4)
+SCENARIO_KEYS = ("n_workers", "batch", "total_samples", "quota_num", "quota_den", "period", "jitter", "sched_seed",
+                 "grad_seed", "slow_worker", "slow_factor", "slow_t0", "slow_t1", "window_ticks", "K")
+
+
+def scenario(sc: dict, state: "Oracle | None" = None, P: int = 0, cap: int = 256):
+    """Runs the config-4 scenario on `state` (fp32 Oracle) or dry. Returns (switch log [(tick, version, to,
+    reason)], result dict)."""
+    L = lib()
+    if not hasattr(L, "_scen"):
+        L.orc_scenario_run.restype = _i64
+        L.orc_scenario_run.argtypes = [_p, _i64, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _u64, _u64, _i32, _i64,
+                                       _i64, _i64, _i64, _i32, _p, _i32, _p]
+        L._scen = True
+    log = np.zeros((cap, 4), dtype=np.int64)
+    res = np.zeros(7, dtype=np.int64)
+    if state is not None:
+        assert state.dtype == np.float32
+    nsw = L.orc_scenario_run(state._h if state is not None else None, P, sc["n_workers"], sc["batch"],
+                             sc["total_samples"], sc["quota_num"], sc["quota_den"], sc["period"], sc["jitter"],
+                             sc["sched_seed"], sc["grad_seed"], sc["slow_worker"], sc["slow_factor"], sc["slow_t0"],
+                             sc["slow_t1"], sc["window_ticks"], sc["K"], _ptr(log), cap, _ptr(res))
+    keys = ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version", "windows", "n_switches")
+    return [tuple(int(x) for x in r) for r in log[:min(nsw, cap)]], dict(zip(keys, (int(x) for x in res)))

@@ -244,3 +244,144 @@ int32_t orc_detector_window(orc_detector *dt, const double *samples, const doubl
   free(Sk);
   return dt->clean_run >= dt->K;
 }
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Online straggler scenario (config 4; DESIGN reading C23), written from its stated rules:
+ *  - ticks are integers; worker j's k-th step lasts T_j(t) + d_{j,k} (T_j = period, x slow_factor for the slow worker
+ *    while slow_t0 <= t < slow_t1; d as in the schedule), t = the time the step starts;
+ *  - BSP superstep: all n workers compute from the same start time; the step ends at the slowest; each worker's busy
+ *    time is its own duration; n*B samples;
+ *  - ASP: each worker's next push happens when its step ends (earliest first, ties by lower id), then it pulls and
+ *    starts its next step; B samples per push;
+ *  - after every event, each detection window that ended at or before the current tick is evaluated in order with
+ *    the samples / busy time of the steps completed inside it, then the greedy rule is applied;
+ *  - the BSP share is the first W*q_num/q_den samples; meeting it switches to ASP for good;
+ *  - a greedy switch back to BSP makes every worker's in-flight gradient arrive late (rejected, counted).
+ * st == NULL: dry run (no data). Gradients: worker j's k-th gradient is orc_synth_grad(grad_seed, j, k, 0, P). */
+int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, int64_t q_num, int64_t q_den,
+                         int64_t period, int64_t jitter, uint64_t sched_seed, uint64_t grad_seed, int32_t slow_worker,
+                         int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t D, int32_t K,
+                         int64_t *log4, int32_t cap, int64_t *res7) {
+  int64_t quota = (W / q_den) * q_num + ((W % q_den) * q_num) / q_den;   /* floor(W * q_num / q_den) */
+  int64_t *steps = (int64_t *)calloc((size_t)n, sizeof(int64_t));      /* gradients computed per worker */
+  int64_t *base = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+  int64_t *finish = (int64_t *)calloc((size_t)n, sizeof(int64_t));     /* ASP: when the running step ends */
+  int64_t *length = (int64_t *)calloc((size_t)n, sizeof(int64_t));     /* ASP: its duration */
+  double *win_samples = (double *)calloc((size_t)n, sizeof(double));
+  double *win_busy = (double *)calloc((size_t)n, sizeof(double));
+  int32_t *flag = (int32_t *)calloc((size_t)n, sizeof(int32_t));
+  float **g = (float **)calloc((size_t)n, sizeof(float *));
+  for (int32_t j = 0; j < n; j++) g[j] = st ? (float *)malloc((size_t)P * sizeof(float)) : NULL;
+  int64_t *ver = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+  int32_t *ids = (int32_t *)calloc((size_t)n, sizeof(int32_t));
+  for (int32_t j = 0; j < n; j++) ids[j] = j;
+  orc_detector *det = orc_detector_new(n, K);
+  int64_t now = 0, processed = 0, bsp_samples = 0, version = 0, next_window = D;
+  int64_t bsp_steps = 0, asp_pushes = 0, dropped = 0, windows = 0, nlog = 0;
+  int32_t proto = ORC_BSP;
+
+#define STEP_LEN(j, at)                                                                                       \
+  ((((j) == slow_worker && (at) >= slow_t0 && (at) < slow_t1) ? period * slow_factor : period) +              \
+   (jitter > 0 ? (int64_t)(orc_splitmix64(sched_seed ^ ((uint64_t)(uint32_t)(j) << 32) ^ (uint64_t)(steps[j] + 1)) % \
+                           (uint64_t)(2 * jitter + 1)) - jitter                                                \
+               : 0))
+#define LOG_SWITCH(to, why)                      \
+  do {                                           \
+    if (st) orcf_switch(st, (to), 0);            \
+    if (nlog < cap) {                            \
+      log4[4 * nlog + 0] = now;                  \
+      log4[4 * nlog + 1] = version;              \
+      log4[4 * nlog + 2] = (to);                 \
+      log4[4 * nlog + 3] = (why);                \
+    }                                            \
+    nlog++;                                      \
+    proto = (to);                                \
+  } while (0)
+#define BEGIN_ASP()                                              \
+  do {                                                           \
+    for (int32_t q = 0; q < n; q++) {                            \
+      if (st) orcf_pull(st, q, NULL, &base[q]);                  \
+      else base[q] = version;                                    \
+      length[q] = STEP_LEN(q, now);                              \
+      finish[q] = now + length[q];                               \
+    }                                                            \
+  } while (0)
+
+  while (processed < W) {
+    if (proto == ORC_BSP) {
+      int64_t slowest = 0;
+      for (int32_t j = 0; j < n; j++) {
+        int64_t len = STEP_LEN(j, now);
+        if (len > slowest) slowest = len;
+        win_busy[j] += (double)len;
+        win_samples[j] += (double)B;
+        if (st) orc_synth_grad(grad_seed, j, steps[j], 0, P, g[j]);
+        ver[j] = version;
+      }
+      if (st) orcf_bsp_step(st, (const float *const *)g, ids, ver, n);
+      for (int32_t j = 0; j < n; j++) steps[j]++;
+      version++;
+      now += slowest;
+      processed += (int64_t)n * B;
+      bsp_samples += (int64_t)n * B;
+      bsp_steps++;
+      if (bsp_samples >= quota) {
+        LOG_SWITCH(ORC_ASP, 0);
+        BEGIN_ASP();
+      }
+    } else {
+      int32_t j = 0;
+      for (int32_t q = 1; q < n; q++)
+        if (finish[q] < finish[j]) j = q;
+      now = finish[j];
+      int64_t stale = 0;
+      if (st) {
+        orc_synth_grad(grad_seed, j, steps[j], 0, P, g[j]);
+        orcf_asp_push(st, j, g[j], base[j], &stale);
+      }
+      steps[j]++;
+      version++;
+      if (st) orcf_pull(st, j, NULL, &base[j]);
+      else base[j] = version;
+      win_busy[j] += (double)length[j];
+      win_samples[j] += (double)B;
+      processed += B;
+      asp_pushes++;
+      length[j] = STEP_LEN(j, now);
+      finish[j] = now + length[j];
+    }
+    while (next_window <= now) {
+      int32_t clean = orc_detector_window(det, win_samples, win_busy, flag);
+      int32_t any = 0;
+      for (int32_t q = 0; q < n; q++) {
+        any |= flag[q];
+        win_samples[q] = 0.0;
+        win_busy[q] = 0.0;
+      }
+      next_window += D;
+      windows++;
+      if (proto == ORC_BSP && any && bsp_samples < quota) {          /* P:1421 straggler during BSP */
+        LOG_SWITCH(ORC_ASP, 1);
+        BEGIN_ASP();
+      } else if (proto == ORC_ASP && clean && bsp_samples < quota) { /* P:1421 clean and BSP unfinished */
+        LOG_SWITCH(ORC_BSP, 2);
+        for (int32_t q = 0; q < n; q++) {
+          if (st) orcf_asp_push(st, q, g[q], base[q], NULL);          /* late: rejected, counted as dropped */
+          steps[q]++;
+          dropped++;
+        }
+      }
+    }
+  }
+#undef STEP_LEN
+#undef LOG_SWITCH
+#undef BEGIN_ASP
+  res7[0] = bsp_steps; res7[1] = asp_pushes; res7[2] = dropped; res7[3] = now; res7[4] = version;
+  res7[5] = windows; res7[6] = nlog;
+  for (int32_t j = 0; j < n; j++) free(g[j]);
+  free(g); free(steps); free(base); free(finish); free(length); free(win_samples); free(win_busy); free(flag);
+  free(ver);
+  free(ids);
+  orc_detector_free(det);
+  return nlog;
+}

@@ -101,6 +101,14 @@ void orc_detector_free(orc_detector *dt);
  * ("cluster free of stragglers", SV C15), else 0. */
 int32_t orc_detector_window(orc_detector *dt, const double *samples, const double *busy, int32_t *straggler);
 
+/* ---- online straggler scenario (config 4): greedy policy over the detector ----
+ * st: an orcf_* state with n workers (NULL: dry run). Writes up to cap switch records {tick, version, to, reason} to
+ * log4 and {bsp_steps, asp_pushes, dropped, end_tick, version, windows, n_switches} to res7. Returns n_switches. */
+int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, int64_t q_num, int64_t q_den,
+                         int64_t period, int64_t jitter, uint64_t sched_seed, uint64_t grad_seed, int32_t slow_worker,
+                         int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t D, int32_t K,
+                         int64_t *log4, int32_t cap, int64_t *res7);
+
 #ifdef __cplusplus
 }
 #endif

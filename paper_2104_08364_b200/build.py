@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsyncswitch.so")
-SOURCES = ["runtime.cu", "kernels.cu", "control.cpp"]
+SOURCES = ["runtime.cu", "kernels.cu", "control.cpp", "scenario.cpp"]
 HEADERS_EXTRA = ["plan.h"]
 HEADERS = ["internal.h", "plan.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

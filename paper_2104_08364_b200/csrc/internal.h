@@ -83,6 +83,14 @@ struct ScatterArgs {
   PeerSync sync;
 };
 
+// What the in-library drivers (scenario.cpp) need to know about a context.
+struct CtxInfo {
+  int64_t P;
+  int32_t n, rank, world, max_window;
+  bool fused;
+  cudaStream_t stream;
+};
+
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s);
@@ -92,4 +100,9 @@ cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, i
 cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
                                 float *grad, float *loss, float *scratch, cudaStream_t s);
 
+}  // namespace ss
+
+struct ss_ctx;
+namespace ss {
+CtxInfo ctx_info(const ss_ctx *c);
 }  // namespace ss

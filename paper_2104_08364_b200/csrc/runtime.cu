@@ -1062,3 +1062,17 @@ ss_status ss_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d
 }
 
 }  // extern "C"
+
+namespace ss {
+CtxInfo ctx_info(const ss_ctx *c) {
+  CtxInfo i;
+  i.P = c->P;
+  i.n = c->n;
+  i.rank = c->rank;
+  i.world = c->world;
+  i.max_window = c->max_win;
+  i.fused = c->fused_mode != 0;
+  i.stream = c->stream;
+  return i;
+}
+}  // namespace ss

@@ -30,7 +30,8 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
-           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer"]
+           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer",
+           "ss_scenario_run"]
 
 
 class SSError(RuntimeError):
@@ -43,6 +44,25 @@ class ss_route_op(ctypes.Structure):
     _fields_ = [("window", ctypes.c_int32), ("phase", ctypes.c_int32), ("op", ctypes.c_int32),
                 ("peer", ctypes.c_int32), ("event", ctypes.c_int32), ("offset", ctypes.c_int64),
                 ("count", ctypes.c_int64)]
+
+
+class ss_scenario(ctypes.Structure):
+    _fields_ = [("n_workers", ctypes.c_int32), ("batch", ctypes.c_int64), ("total_samples", ctypes.c_int64),
+                ("quota_num", ctypes.c_int64), ("quota_den", ctypes.c_int64), ("period", ctypes.c_int64),
+                ("jitter", ctypes.c_int64), ("sched_seed", ctypes.c_uint64), ("grad_seed", ctypes.c_uint64),
+                ("slow_worker", ctypes.c_int32), ("slow_factor", ctypes.c_int64), ("slow_t0", ctypes.c_int64),
+                ("slow_t1", ctypes.c_int64), ("window_ticks", ctypes.c_int64), ("K", ctypes.c_int32)]
+
+
+class ss_switch_event(ctypes.Structure):
+    _fields_ = [("tick", ctypes.c_int64), ("version", ctypes.c_int64), ("to_protocol", ctypes.c_int32),
+                ("reason", ctypes.c_int32)]
+
+
+class ss_scenario_result(ctypes.Structure):
+    _fields_ = [("bsp_steps", ctypes.c_int64), ("asp_pushes", ctypes.c_int64), ("dropped", ctypes.c_int64),
+                ("end_tick", ctypes.c_int64), ("version", ctypes.c_int64), ("windows", ctypes.c_int64),
+                ("n_switches", ctypes.c_int32)]
 
 
 class ss_event(ctypes.Structure):
@@ -88,6 +108,7 @@ def _load():
         "ss_detector_new": [p, i32, i32],
         "ss_detector_window": [p, p, p, p, p],
         "ss_route_plan": [i32, i32, i32, i32, i64, i32, i32, p, p, i64, p, i64, p, p],
+        "ss_scenario_run": [p, p, p, p, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -313,6 +334,18 @@ def ss_route_plan(rank: int, world: int, n_workers: int, n_shards: int, n_params
                           ctypes.byref(nwin))
     ops = [(o.window, o.phase, o.op, o.peer, o.event, o.offset, o.count) for o in arr[:total.value]]
     return s, ops, nwin.value
+
+
+def ss_scenario_run(ctx, sc: dict, cap: int = 256):
+    """Config-4 scenario on a context (or ctx=None: host-only dry run). Returns (status, switch log
+    [(tick, version, to, reason)], result dict)."""
+    c = ss_scenario(**sc)
+    log = (ss_switch_event * cap)()
+    out = ss_scenario_result()
+    s = lib.ss_scenario_run(ctx, ctypes.byref(c), ctypes.byref(out), ctypes.cast(log, ctypes.c_void_p), cap)
+    res = {k: getattr(out, k) for k, _ in ss_scenario_result._fields_}
+    entries = [(e.tick, e.version, e.to_protocol, e.reason) for e in log[:min(out.n_switches, cap)]]
+    return s, entries, res
 
 
 class Detector:
