@@ -166,24 +166,50 @@ def run_ours(args):
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(g.stream)
 
-    def step(grad_src, dst_src):
-        ver = g.version
-        g.bsp_step([grad_src[(j, 0)] for j in hosted], hosted, [ver] * len(hosted))
-        g.switch(ss.SS_ASP, 0)
-        base = ver + 1
-        for j in range(n):
-            st = g.asp_push(j, grad_src.get((j, 1)), base)
-            assert st == j
-            g.pull(j, dst_src.get(j))
-        g.switch(ss.SS_BSP, 0)
+    class Step:
+        """One bench step through the C-ABI with prebuilt argument arrays: ss_bsp_step, ss_switch(ASP),
+        ss_asp_replay(n pushes, each followed by its pull), ss_switch(BSP) — four C calls per step.
+        `mark` (optional) is recorded on the library's stream between the BSP and the ASP phase."""
+
+        def __init__(self, grad_src, dst_src):
+            import ctypes
+            self.ct = ctypes
+            self.k = len(hosted)
+            self.gp = (ctypes.c_void_p * max(self.k, 1))(*[ss.ptr(grad_src[(j, 0)]) for j in hosted])
+            self.ws = np.array(hosted, dtype=np.int32)
+            self.vs = np.zeros(max(self.k, 1), dtype=np.int64)
+            self.ev = (ss.ss_event * (2 * n))()
+            for j in range(n):
+                self.ev[2 * j] = ss.ss_event(0, j, 0, ss.ptr(grad_src.get((j, 1))), None)
+                self.ev[2 * j + 1] = ss.ss_event(1, j, 0, None, ss.ptr(dst_src.get(j)))
+            self.gp_c = ctypes.cast(self.gp, ctypes.c_void_p)
+            self.ev_c = ctypes.cast(self.ev, ctypes.c_void_p)
+
+        def __call__(self, ver, mark=None):
+            L, c = ss.lib, g.ctx
+            self.vs[:] = ver
+            for j in range(n):
+                self.ev[2 * j].version = ver + 1
+            s = L.ss_bsp_step(c, self.gp_c, self.ws.ctypes.data, self.vs.ctypes.data, self.k)
+            if mark is not None:
+                mark.record(stream)
+            s = s or L.ss_switch(c, ss.SS_ASP, 0)
+            s = s or L.ss_asp_replay(c, self.ev_c, 2 * n, None)
+            s = s or L.ss_switch(c, ss.SS_BSP, 0)   # takes effect at once: flushes the ASP window
+            if s:
+                raise ss.SSError(s, g.last_error())
+            return ver + 1 + n
+
+    step_dev = Step(ring, pull_dst)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    ver = g.version
     for _ in range(args.warmup):
-        step(ring, pull_dst)
+        ver = step_dev(ver)
     barrier()
 
     clocks = Clocks(local)
@@ -194,15 +220,7 @@ def run_ours(args):
     barrier()
     ev[0].record(stream)
     for k in range(args.steps):
-        ver = g.version
-        g.bsp_step([ring[(j, 0)] for j in hosted], hosted, [ver] * len(hosted))
-        ev[2 * k + 1].record(stream)
-        g.switch(ss.SS_ASP, 0)
-        for j in range(n):
-            g.asp_push(j, ring.get((j, 1)), ver + 1)
-            g.pull(j, pull_dst.get(j))
-        g.switch(ss.SS_BSP, 0)
-        g.stats(1)                     # resolves the switch back (flushes the ASP window) inside the step
+        ver = step_dev(ver, mark=ev[2 * k + 1])
         ev[2 * k + 2].record(stream)
     barrier()
     clk = clocks.stop()
@@ -229,13 +247,14 @@ def run_ours(args):
         hdst = {j: torch.empty(P, pin_memory=True) for j in hosted}
         del ring
         torch.cuda.empty_cache()
-        step(hring, hdst)
+        step_host = Step(hring, hdst)
+        ver = step_host(ver)
         g.sync()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            step(hring, hdst)
+            ver = step_host(ver)
             g.sync()                   # the step's results (pull snapshots) are on the host
         e1.record(stream)
         barrier()
@@ -265,7 +284,7 @@ def run_ours(args):
             gbs = k["bytes"] / (k["ms"] / 1e3) / 1e9
             kernels[name] = {"launches": k["launches"], "avg_us": round(1e3 * k["ms"] / k["launches"], 2),
                              "GBps": round(gbs, 1), "frac": round(gbs / hbm_peak, 4),
-                             "share_of_step": round(k["ms"] / (total_ms * (1 if world == 1 else 1)), 4)}
+                             "share_of_step": round(k["ms"] / total_ms, 4)}
 
     steps_per_s = args.steps / (total_ms / 1e3)
     phases = {"bsp_steps_per_s": args.steps / (bsp_ms / 1e3), "asp_pushes_per_s": n * args.steps / (asp_ms / 1e3),

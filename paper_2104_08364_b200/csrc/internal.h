@@ -95,6 +95,7 @@ cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
+cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s);
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
                               cudaStream_t s);
 cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,

@@ -14,6 +14,7 @@
 // v = fma(mu, v, g), w = fma(-eta, v, w).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -343,6 +344,154 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------------------------------------------
+// K2, TMA form: the same replay, with every push's gradient tile staged through a shared-memory ring filled by 1-D
+// bulk copies (cp.async.bulk, completion on an mbarrier). One CTA walks its tiles (kTmaTile floats = 8 KB); the w and
+// v of a tile live in registers for the whole window; thread 0 keeps kTmaStages tile loads in flight ahead of the
+// consumers, across push and tile boundaries, so the bytes in flight no longer depend on registers per thread.
+constexpr int kTmaTile = 2048;                       // floats per tile: 256 threads x 2 float4
+constexpr int kTmaStages = 6;
+constexpr int kTmaSmem = kTmaStages * kTmaTile * 4;  // 48 KB of dynamic shared memory
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
+  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ int push_ev[kMaxEvents];
+  __shared__ int n_push_s;
+  const float mu = a.mu, lam = a.lam;
+  if (threadIdx.x == 0) {
+    int np = 0;
+    for (int e = 0; e < a.n_ev; ++e)
+      if (a.ev[e].kind == 0) push_ev[np++] = e;
+    n_push_s = np;
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int n_push = n_push_s;
+  const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
+  const int64_t n_tiles = (nvec + kTmaTile - 1) / kTmaTile;
+  const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = my_tiles * n_push;                   // one gradient tile per (tile, push)
+
+  auto issue = [&](int64_t it) {                             // thread 0: stage the gradient tile of item `it`
+    const int64_t tile = blockIdx.x + (it / n_push) * gridDim.x;
+    const int64_t off = tile * kTmaTile;
+    const int64_t len = min((int64_t)kTmaTile, nvec - off);
+    const int s = (int)(it % kTmaStages);
+    mbar_expect_tx(&full[s], (uint32_t)(len * 4));
+    bulk_g2s(ring + s * kTmaTile, a.ev[push_ev[it % n_push]].src + off, (uint32_t)(len * 4), &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t it = 0; it < items && it < kTmaStages; ++it) issue(it);
+
+  bool bad = false;
+  int64_t it = 0;
+  for (int64_t tl = 0; tl < my_tiles; ++tl) {
+    const int64_t off = (blockIdx.x + tl * gridDim.x) * kTmaTile;
+    const int64_t len = min((int64_t)kTmaTile, nvec - off);
+    float4 wv[2], vv[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = 4 * (threadIdx.x + u * kThreads);    // element within the tile
+      ok[u] = i < len;
+      if (ok[u]) {
+        wv[u] = ld4(a.w + off + i);
+        vv[u] = ld4(a.v + off + i);
+      }
+    }
+    for (int e = 0; e < a.n_ev; ++e) {
+      if (a.ev[e].kind == 0) {
+        const int s = (int)(it % kTmaStages);
+        mbar_wait(&full[s], (uint32_t)((it / kTmaStages) & 1));
+        const float neg_eta = -a.ev[e].lr;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+          float4 g = *reinterpret_cast<const float4 *>(ring + s * kTmaTile + 4 * (threadIdx.x + u * kThreads));
+          float *gp = &g.x, *wp = &wv[u].x, *vp = &vv[u].x;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float gg = gp[c];
+            if (lam != 0.0f) gg = __fmaf_rn(lam, wp[c], gg);   // g + f(w) at the PS's current w
+            vp[c] = __fmaf_rn(mu, vp[c], gg);
+            wp[c] = __fmaf_rn(neg_eta, vp[c], wp[c]);
+          }
+        }
+        __syncthreads();                                        // every thread is done with stage s
+        if (threadIdx.x == 0 && it + kTmaStages < items) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(it + kTmaStages);
+        }
+        ++it;
+      } else if (a.ev[e].dst != nullptr) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (ok[u]) st4(a.ev[e].dst + off + 4 * (threadIdx.x + u * kThreads), wv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
+             nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
+      const int64_t i = off + 4 * (threadIdx.x + u * kThreads);
+      st4(a.w + i, wv[u]);
+      st4(a.v + i, vv[u]);
+    }
+  }
+  // scalar tail (count % 4 elements), first CTA
+  if (blockIdx.x == 0) {
+    const int64_t i = nvec + threadIdx.x;
+    if (i < a.count) {
+      float w = a.w[i], v = a.v[i];
+      for (int e = 0; e < a.n_ev; ++e) {
+        if (a.ev[e].kind == 0) {
+          float gg = a.ev[e].src[i];
+          if (lam != 0.0f) gg = __fmaf_rn(lam, w, gg);
+          v = __fmaf_rn(mu, v, gg);
+          w = __fmaf_rn(-a.ev[e].lr, v, w);
+        } else if (a.ev[e].dst) {
+          a.ev[e].dst[i] = w;
+        }
+      }
+      bad |= nonfinite(w) | nonfinite(v);
+      a.w[i] = w;
+      a.v[i] = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+  peer_done(a.sync);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
 // scatter (fused path): every hosted gradient's owner slices go to the owners' inboxes with
 // posted 128-bit NVLink stores (the local slice is read in place by the owner update, never copied).
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
@@ -376,6 +525,53 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
       const int64_t r = i / a.reg_len;
       if (r != me) a.inbox[r][slot_off + (i - r * a.reg_len)] = src[i];
     }
+  }
+  peer_done(a.sync);
+}
+
+// scatter_sum (fused mode 2): one pass over the hosted gradients — sum them in ascending order and store each owner's
+// slice of the pre-sum straight into that owner's inbox slot a.slot[0] (this rank's id); the own slice stays local.
+__global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = a.P >> 2, reg4 = a.reg_len >> 2;
+  const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
+  constexpr int U = 2;
+  for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < n4 && a.n_src > 0) acc[u] = ld4(a.src[0] + 4 * q);
+    }
+    for (int j0 = 1; j0 < a.n_src; j0 += kG1) {
+      float4 t[kG1][U];
+#pragma unroll
+      for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + jj < a.n_src && q0 + u * stride < n4) t[jj][u] = ld4(a.src[j0 + jj] + 4 * (q0 + u * stride));
+#pragma unroll
+      for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + jj < a.n_src && q0 + u * stride < n4) acc[u] = add4(acc[u], t[jj][u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      if (q >= n4) continue;
+      const int64_t r = q / reg4;
+      *reinterpret_cast<float4 *>(a.inbox[r] + slot_off + 4 * (q - r * reg4)) = acc[u];
+    }
+  }
+  const int64_t i = 4 * n4 + tid;  // scalar tail
+  if (i < a.P) {
+    float acc = a.n_src > 0 ? a.src[0][i] : 0.0f;
+    for (int j = 1; j < a.n_src; ++j) acc = __fadd_rn(acc, a.src[j][i]);
+    const int64_t r = i / a.reg_len;
+    a.inbox[r][slot_off + (i - r * a.reg_len)] = acc;
   }
   peer_done(a.sync);
 }
@@ -494,11 +690,20 @@ int num_sms() {
 
 // Grid: enough CTAs for the work, capped at (resident CTAs per SM) x (SM count) — one full wave of a persistent
 // grid-stride kernel (B200: 148 SMs).
+// Resident CTAs per SM, queried once per kernel (a host API call per launch would dominate small launches).
+template <typename K>
+int resident_ctas(K kernel) {
+  static int r = 0;
+  if (r == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
+    if (r <= 0) r = 1;
+  }
+  return r;
+}
+
 template <typename K>
 int grid_for(K kernel, int64_t work_items) {
-  int r = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
-  const int resident = r > 0 ? r : 1;
+  const int resident = resident_ctas(kernel);
   int64_t want = (work_items + kThreads - 1) / kThreads;
   int64_t cap = (int64_t)resident * num_sms();
   if (want < 1) want = 1;
@@ -533,13 +738,36 @@ cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
 
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   if ((a.count <= 0 || a.n_ev <= 0) && a.sync.wait_epoch == 0 && a.sync.signal_epoch == 0) return cudaSuccess;
-  if (vec) {
+  static const int variant = [] {  // SS_ASP_KERNEL=reg selects the register-prefetch form (A/B measurement)
+    const char *e = getenv("SS_ASP_KERNEL");
+    return (e && e[0] == 'r') ? 0 : 1;
+  }();
+  if (vec && variant == 1) {
+    auto k = asp_replay_tma_kernel;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      attr = true;
+    }
+    static int r = 0;
+    if (r == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k, kThreads, kTmaSmem);
+    const int64_t tiles = ((a.count >> 2) * 4 + kTmaTile - 1) / kTmaTile;
+    int64_t grid = (int64_t)(r > 0 ? r : 1) * num_sms();
+    if (tiles < grid) grid = tiles > 0 ? tiles : 1;
+    k<<<(int)grid, kThreads, kTmaSmem, s>>>(a);
+  } else if (vec) {
     auto k = asp_replay_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);
   } else {
     auto k = asp_replay_kernel<false>;
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
+  auto k = scatter_sum_kernel;
+  k<<<grid_for(k, (a.P / 4 + 1) / 2 + 1), kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

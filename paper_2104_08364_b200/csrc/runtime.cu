@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "internal.h"
@@ -103,6 +104,7 @@ struct ss_ctx {
   // instrumentation
   bool prof = false;
   std::vector<Timed> timed;
+  std::vector<cudaEvent_t> event_pool;
   KStat kstat[4];
   std::string err;
 };
@@ -142,13 +144,19 @@ ss_status fail(ss_ctx *c, ss_status s, const char *fmt, ...) {
     if (s_ != SS_OK) return s_;   \
   } while (0)
 
+// Device or host memory? UVA keeps device and host virtual ranges disjoint while the context lives, so a pointer
+// once seen as device memory stays device memory: remember those (the query costs ~1 us per call).
 bool is_host_ptr(const void *p) {
+  static thread_local std::unordered_set<const void *> device_seen;
+  if (device_seen.count(p)) return false;
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return true;
   }
-  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+  const bool host = at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+  if (!host && device_seen.size() < 4096) device_seen.insert(p);
+  return host;
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -200,12 +208,23 @@ ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
   return SS_OK;
 }
 
+cudaEvent_t pooled_event(ss_ctx *c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
 void timed_begin(ss_ctx *c, Timed *t, int kernel, double bytes) {
   if (!c->prof) return;
   t->kernel = kernel;
   t->bytes = bytes;
-  cudaEventCreate(&t->a);
-  cudaEventCreate(&t->b);
+  t->a = pooled_event(c);
+  t->b = pooled_event(c);
   cudaEventRecord(t->a, c->stream);
 }
 
@@ -224,8 +243,8 @@ ss_status drain_timed(ss_ctx *c) {
     c->kstat[t.kernel].launches += 1;
     c->kstat[t.kernel].ms += ms;
     c->kstat[t.kernel].bytes += t.bytes;
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
+    c->event_pool.push_back(t.a);
+    c->event_pool.push_back(t.b);
   }
   c->timed.clear();
   return SS_OK;
@@ -662,6 +681,7 @@ void ss_destroy(ss_ctx *c) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   close_ipc(c, true);
   if (c->comm) ncclCommDestroy(c->comm);
   for (float *p : c->stage) cudaFree(p);
@@ -766,32 +786,32 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     const int64_t lo = c->real_lo[me], cnt = c->real_hi[me] - lo;
     std::vector<std::pair<const float *, int32_t>> src;
     if (presum) {
-      if (k > 0) {
-        ss::SumArgs sa;
-        std::memset(&sa, 0, sizeof sa);
-        for (int32_t i = 0; i < k; ++i) sa.g[i] = a.g[i];
-        sa.n_in = k;
-        sa.out = c->sum_buf;
-        sa.count = c->P;
-        sa.count_pad = c->P_pad;
-        Timed t;
-        timed_begin(c, &t, 2, 4.0 * ((double)c->P * k + (double)c->P_pad));
-        SS_CUDA(c, ss::launch_local_sum(sa, vec, c->stream));
-        timed_end(c, &t);
-      } else {
-        SS_CUDA(c, cudaMemsetAsync(c->sum_buf, 0, (size_t)c->P_pad * sizeof(float), c->stream));
+      // one pass: pre-sum of the hosted gradients, each owner's slice stored into its inbox slot `me`
+      ss::ScatterArgs sa;
+      std::memset(&sa, 0, sizeof sa);
+      sa.n_src = k;
+      for (int32_t i = 0; i < k; ++i) {
+        sa.src[i] = a.g[i];
+        if (!aligned16(a.g[i])) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
       }
-      src.push_back({c->sum_buf, me});
+      sa.slot[0] = me;
+      for (int32_t q = 0; q < c->world; ++q) sa.inbox[q] = c->peer_inbox[q];
+      sa.reg_len = c->reg_len;
+      sa.P = c->P;
+      sa.sync = peer_sync(c, 0, epA, false);
+      Timed t;
+      timed_begin(c, &t, 3, 4.0 * (double)c->P * (k + 1));
+      SS_CUDA(c, ss::launch_scatter_sum(sa, c->stream));
+      timed_end(c, &t);
     } else {
       for (int32_t i = 0; i < k; ++i) src.push_back({a.g[i], c->first_hosted + i});
+      SS_TRY(launch_scatter(c, src, epA));
     }
-    SS_TRY(launch_scatter(c, src, epA));
     const float *hosted_g[ss::kMaxWorkers];
     for (int32_t i = 0; i < k; ++i) hosted_g[i] = a.g[i];
     std::memset(a.g, 0, sizeof a.g);
     if (presum) {
-      for (int32_t q = 0; q < c->world; ++q)
-        a.g[q] = q == me ? c->sum_buf + lo : c->inbox + (int64_t)q * c->reg_len;
+      for (int32_t q = 0; q < c->world; ++q) a.g[q] = c->inbox + (int64_t)q * c->reg_len;
       a.n_in = c->world;
     } else {
       for (int32_t j = 0; j < c->n; ++j)
