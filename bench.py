@@ -36,7 +36,14 @@ CONFIGS = {
                                                      "n=8 workers, S=8 shards"),
     "5a": dict(P=100_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=1e8 fp32, n=S=8"),
     "5b": dict(P=250_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=2.5e8 fp32, n=S=8"),
+    "5c": dict(P=500_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=5e8 fp32, n=S=8"),
+    "5d": dict(P=1_000_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=1e9 fp32, n=S=8"),
+    "4": dict(P=25_557_032, n=8, S=8, window=16, name="config4: ASP straggler scenario, worker 7 4x slow for "
+              "100,000 ticks during BSP, greedy switching (P:1421), P=25,557,032, n=S=8"),
 }
+SCENARIO4 = dict(n_workers=8, batch=128, total_samples=64000 * 128, quota_num=1, quota_den=4, period=1000, jitter=0,
+                 sched_seed=7, grad_seed=20241018, slow_worker=7, slow_factor=4, slow_t0=20000, slow_t1=120000,
+                 window_ticks=10000, K=3)
 METRIC = "BSP sync steps/s and ASP pushes/s at 1/2/4/8 B200; HBM & NVLink GB/s vs peak"
 UNIT = "steps/s (1 step = 1 BSP superstep + switch + n ASP push/pull + switch)"
 SEED = 20241018
@@ -48,6 +55,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
+    ap.add_argument("--scenario-samples", type=int, default=16000 * 128,
+                    help="config 4: total samples W of the scenario (the paper's 64K x 128 takes minutes)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fused", default="auto", choices=["auto", "0", "1", "2"],
                     help="G>1 exchange: 0 NCCL, 1 fused exact, 2 fused pre-summed; auto = 1 if n <= G else 2")
@@ -322,6 +331,46 @@ def run_ours(args):
 
 
 # ------------------------------------------------------------------------------------------------------------------
+def run_scenario(args):
+    """Config 4: the online straggler scenario (ss_scenario_run) on 1 GPU; device time by CUDA events around the run.
+    Reports protocol updates/s (BSP steps + ASP pushes per second, gradients generated in-line by synth_grad as the
+    worker stand-in), the switch log, the staleness histogram and the dropped pushes."""
+    import torch
+    from paper_2104_08364_b200 import syncswitch as ss
+    cfg = CONFIGS["4"]
+    P, n, S = cfg["P"], cfg["n"], cfg["S"]
+    sc = dict(SCENARIO4, total_samples=args.scenario_samples)
+    w0 = torch.empty(P, device="cuda")
+    ss.ss_check(ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0))
+    w0.mul_(64.0)
+    torch.cuda.synchronize()
+    g = ss.SyncSwitch(w0, S, n, 0.1, 0.9)
+    g.set_window(cfg["window"])
+    stream = torch.cuda.ExternalStream(g.stream)
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    s, log, res = ss.ss_scenario_run(g.ctx, sc)
+    e1.record(stream)
+    g.sync()
+    clk = clocks.stop()
+    assert s == 0, g.last_error()
+    ms = e0.elapsed_time(e1)
+    st = g.stats(64)
+    updates = res["bsp_steps"] + res["asp_pushes"]
+    line = {"metric": METRIC, "value": round(updates / (ms / 1e3), 1),
+            "unit": "protocol updates/s (BSP steps + ASP pushes, scenario incl. in-line gradient generation)",
+            "n_gpus": 1, "steps": updates, "warmup": 0, "ms_per_step": ms / updates, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash gradients)",
+            "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "scenario": sc},
+            "scenario": {"switches": [dict(zip(("tick", "version", "to", "reason"), e)) for e in log], **res,
+                         "staleness_hist": {str(i): int(x) for i, x in enumerate(st["hist"]) if x}},
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
 def _oracle_step(orc, o, n, grads_bsp, grads_asp):
     ver = o.version
     assert o.bsp_step(grads_bsp, versions=[ver] * n) == 0
@@ -408,5 +457,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == "4":
+        run_scenario(a)
     else:
         run_ours(a)
