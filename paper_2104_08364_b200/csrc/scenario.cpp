@@ -19,10 +19,14 @@ uint64_t mix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+// Gradient ring and pull destinations of the run. Buffers passed to the protocol calls are borrowed until ss_sync
+// (an ASP window may still reference them), so the ring is released only after a flush + sync, on every exit path.
 struct Buffers {
+  ss_ctx *ctx = nullptr;
   std::vector<float *> bsp, asp, pull;
   std::vector<float *> owned;
   ~Buffers() {
+    if (ctx) ss_sync(ctx);
     for (float *p : owned) cudaFree(p);
   }
 };
@@ -47,6 +51,7 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
 
   // device buffers: one BSP gradient per hosted worker, a ring of max_window ASP gradients, a pull destination
   Buffers buf;
+  buf.ctx = ctx;
   if (ctx) {
     auto alloc = [&](std::vector<float *> &v, int32_t count) -> bool {
       for (int32_t i = 0; i < count; ++i) {
