@@ -116,6 +116,23 @@ ss_status ss_set_lr_schedule(ss_ctx *ctx, const int64_t *boundaries, const float
  * added to each gradient at apply time at the PS's current w ("g11 + f(w0)"). Errors: SS_E_INVAL. */
 ss_status ss_set_lr_policy(ss_ctx *ctx, int32_t asp_rule, float weight_decay);
 
+/* Post-switch momentum policy for ASP pushes (SV §8(f) NEXT-4; "setting the momentum to 0 ...
+ * to 1/n ... ramping up the momentum based on 2^i/n ... based on i/n where i is the number of epochs after switching.
+ * Both (iii) and (iv) will stop the ramp up once the momentum reaches the original value used by BSP"):
+ *   rule 0: same momentum as BSP (default; the paper's chosen policy)   rule 1: 0   rule 2: 1/n
+ *   rule 3: 2^i/n   rule 4: i/n,   all capped at the BSP momentum (DESIGN reading C24),
+ * with i = floor(pushes since the last switch to ASP * batch / samples_per_epoch). Computed per push in double and
+ * rounded to fp32 once; BSP supersteps always use the BSP momentum. Errors: SS_E_INVAL. */
+ss_status ss_set_momentum_policy(ss_ctx *ctx, int32_t rule, int64_t samples_per_epoch, int64_t batch);
+
+/* BSP barrier set for the elastic straggler policy (SV §8(f) NEXT-2; "removes any detected stragglers from the
+ * current cluster so as to complete the specified amount of BSP training free of stragglers. Once the designated BSP
+ * workload is fulfilled, it will then restore the cluster size"). workers: `count` distinct ids in [0, n). Later
+ * BSP supersteps expect exactly these workers' gradients; the aggregate is their mean in ascending worker order and
+ * the BSP lr is count*eta (configuration policy re-derived for the smaller cluster). ASP is unaffected.
+ * Restore with all n ids. Collective when distributed. Errors: SS_E_INVAL (empty, duplicate, out of range). */
+ss_status ss_set_members(ss_ctx *ctx, const int32_t *workers, int32_t count);
+
 /* lr used for the next update under `protocol`: (float)((double)eta * factor(version) * scale(protocol)). */
 ss_status ss_current_lr(ss_ctx *ctx, int32_t protocol, float *lr_out);
 
@@ -241,6 +258,10 @@ typedef struct ss_detector ss_detector;
 ss_status ss_detector_new(ss_detector **out, int32_t n, int32_t K);
 ss_status ss_detector_window(ss_detector *dt, const double *samples, const double *busy, int32_t *straggler,
                              int32_t *clean_out);
+/* Same over the workers with mask[k] != 0 only (elastic policy: removed workers are neither measured nor flagged;
+ * their consecutive-window counters restart). mask NULL = all workers. */
+ss_status ss_detector_window_masked(ss_detector *dt, const double *samples, const double *busy, const uint8_t *mask,
+                                    int32_t *straggler, int32_t *clean_out);
 void ss_detector_free(ss_detector *dt);
 
 /* Multi-GPU routing plan (SV §8(a) a8/a10, §8(e)) of an ASP event sequence as rank `rank` of `world` executes it:
@@ -284,10 +305,14 @@ typedef struct {
   int64_t slow_factor, slow_t0, slow_t1;
   int64_t window_ticks;   /* detection window D */
   int32_t K;              /* consecutive windows */
+  int32_t policy;         /* 0: greedy; 1: elastic (stragglers leave the BSP barrier set until the
+                             BSP quota is met, then all workers are restored and ASP runs the rest); 2: none */
 } ss_scenario;
 typedef struct {
   int64_t tick, version;
-  int32_t to_protocol, reason; /* reason 0: BSP quota met (timing policy), 1: straggler (greedy), 2: clean (greedy) */
+  int32_t to_protocol, reason; /* reason 0: BSP quota met (timing policy), 1: straggler (greedy), 2: clean (greedy),
+                                  3: elastic removal of stragglers from the BSP set (no protocol change) */
+  int32_t members;             /* BSP members after the event */
 } ss_switch_event;
 typedef struct {
   int64_t bsp_steps, asp_pushes, dropped, end_tick, version, windows;

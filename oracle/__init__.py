@@ -69,6 +69,10 @@ def lib():
         g("set_lr_schedule").argtypes = [_p, _p, _p, _i32]
         g("set_lr_policy").restype = _i32
         g("set_lr_policy").argtypes = [_p, _i32, _f32]
+        g("set_members").restype = _i32
+        g("set_members").argtypes = [_p, _p, _i32]
+        g("set_momentum_policy").restype = _i32
+        g("set_momentum_policy").argtypes = [_p, _i32, _i64, _i64]
         g("bsp_step").restype = _i32
         g("bsp_step").argtypes = [_p, _p, _p, _p, _i32]
         g("asp_push").restype = _i32
@@ -189,6 +193,13 @@ class Oracle:
     def set_lr_policy(self, asp_rule: int, weight_decay: float) -> int:
         return int(self._fn("set_lr_policy")(self._h, asp_rule, weight_decay))
 
+    def set_members(self, workers) -> int:
+        w = np.ascontiguousarray(workers, dtype=np.int32)
+        return int(self._fn("set_members")(self._h, _ptr(w), w.size))
+
+    def set_momentum_policy(self, rule: int, samples_per_epoch: int = 1, batch: int = 1) -> int:
+        return int(self._fn("set_momentum_policy")(self._h, rule, samples_per_epoch, batch))
+
     def bsp_step(self, grads, workers=None, versions=None) -> int:
         gs = [np.ascontiguousarray(g, dtype=self.dtype) for g in grads]
         if workers is None:
@@ -307,25 +318,26 @@ class Detector:
 # ---------------------------------------------------------------------------------------------------------------
 # online straggler scenario (config 4)
 SCENARIO_KEYS = ("n_workers", "batch", "total_samples", "quota_num", "quota_den", "period", "jitter", "sched_seed",
-                 "grad_seed", "slow_worker", "slow_factor", "slow_t0", "slow_t1", "window_ticks", "K")
+                 "grad_seed", "slow_worker", "slow_factor", "slow_t0", "slow_t1", "window_ticks", "K", "policy")
 
 
 def scenario(sc: dict, state: "Oracle | None" = None, P: int = 0, cap: int = 256):
     """Runs the config-4 scenario on `state` (fp32 Oracle) or dry. Returns (switch log [(tick, version, to,
-    reason)], result dict)."""
+    reason, members)], result dict)."""
     L = lib()
     if not hasattr(L, "_scen"):
         L.orc_scenario_run.restype = _i64
         L.orc_scenario_run.argtypes = [_p, _i64, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _u64, _u64, _i32, _i64,
-                                       _i64, _i64, _i64, _i32, _p, _i32, _p]
+                                       _i64, _i64, _i64, _i32, _i32, _p, _i32, _p]
         L._scen = True
-    log = np.zeros((cap, 4), dtype=np.int64)
+    log = np.zeros((cap, 5), dtype=np.int64)
     res = np.zeros(7, dtype=np.int64)
     if state is not None:
         assert state.dtype == np.float32
     nsw = L.orc_scenario_run(state._h if state is not None else None, P, sc["n_workers"], sc["batch"],
                              sc["total_samples"], sc["quota_num"], sc["quota_den"], sc["period"], sc["jitter"],
                              sc["sched_seed"], sc["grad_seed"], sc["slow_worker"], sc["slow_factor"], sc["slow_t0"],
-                             sc["slow_t1"], sc["window_ticks"], sc["K"], _ptr(log), cap, _ptr(res))
+                             sc["slow_t1"], sc["window_ticks"], sc["K"], sc.get("policy", 0), _ptr(log), cap,
+                             _ptr(res))
     keys = ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version", "windows", "n_switches")
     return [tuple(int(x) for x in r) for r in log[:min(nsw, cap)]], dict(zip(keys, (int(x) for x in res)))

@@ -221,21 +221,25 @@ void orc_detector_free(orc_detector *dt) {
   free(dt);
 }
 
-int32_t orc_detector_window(orc_detector *dt, const double *samples, const double *busy, int32_t *straggler) {
-  int32_t n = dt->n;
+/* With a mask (elastic policy) only the workers still at the BSP barrier are measured: S and sigma are taken over
+ * them, only they can be flagged, the others' consecutive counts restart. */
+int32_t orc_detector_window_masked(orc_detector *dt, const double *samples, const double *busy, const uint8_t *mask,
+                                   int32_t *straggler) {
+  int32_t n = dt->n, counted = 0;
   double *Sk = (double *)malloc((size_t)n * sizeof(double));
   double mean = 0.0;
   for (int32_t k = 0; k < n; k++) {
     Sk[k] = busy[k] > 0.0 ? samples[k] / busy[k] : 0.0;
-    mean += Sk[k];
+    if (mask == NULL || mask[k]) { mean += Sk[k]; counted++; }
   }
-  mean /= (double)n;
+  if (counted > 0) mean /= (double)counted;
   double var = 0.0;
-  for (int32_t k = 0; k < n; k++) var += (Sk[k] - mean) * (Sk[k] - mean);
-  double sigma = sqrt(var / (double)n);
+  for (int32_t k = 0; k < n; k++)
+    if (mask == NULL || mask[k]) var += (Sk[k] - mean) * (Sk[k] - mean);
+  double sigma = counted > 0 ? sqrt(var / (double)counted) : 0.0;
   int32_t any = 0;
   for (int32_t k = 0; k < n; k++) {
-    int32_t flagged = Sk[k] < mean - sigma;
+    int32_t flagged = (mask == NULL || mask[k]) && Sk[k] < mean - sigma;
     dt->run[k] = flagged ? dt->run[k] + 1 : 0;
     straggler[k] = dt->run[k] >= dt->K;
     any |= flagged;
@@ -243,6 +247,10 @@ int32_t orc_detector_window(orc_detector *dt, const double *samples, const doubl
   dt->clean_run = any ? 0 : dt->clean_run + 1;
   free(Sk);
   return dt->clean_run >= dt->K;
+}
+
+int32_t orc_detector_window(orc_detector *dt, const double *samples, const double *busy, int32_t *straggler) {
+  return orc_detector_window_masked(dt, samples, busy, NULL, straggler);
 }
 
 /* ------------------------------------------------------------------------------------------------------------
@@ -261,7 +269,7 @@ int32_t orc_detector_window(orc_detector *dt, const double *samples, const doubl
 int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, int64_t q_num, int64_t q_den,
                          int64_t period, int64_t jitter, uint64_t sched_seed, uint64_t grad_seed, int32_t slow_worker,
                          int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t D, int32_t K,
-                         int64_t *log4, int32_t cap, int64_t *res7) {
+                         int32_t policy, int64_t *log5, int32_t cap, int64_t *res7) {
   int64_t quota = (W / q_den) * q_num + ((W % q_den) * q_num) / q_den;   /* floor(W * q_num / q_den) */
   int64_t *steps = (int64_t *)calloc((size_t)n, sizeof(int64_t));      /* gradients computed per worker */
   int64_t *base = (int64_t *)calloc((size_t)n, sizeof(int64_t));
@@ -274,7 +282,9 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
   for (int32_t j = 0; j < n; j++) g[j] = st ? (float *)malloc((size_t)P * sizeof(float)) : NULL;
   int64_t *ver = (int64_t *)calloc((size_t)n, sizeof(int64_t));
   int32_t *ids = (int32_t *)calloc((size_t)n, sizeof(int32_t));
-  for (int32_t j = 0; j < n; j++) ids[j] = j;
+  uint8_t *active = (uint8_t *)malloc((size_t)n);       /* elastic: workers still at the BSP barrier */
+  for (int32_t j = 0; j < n; j++) active[j] = 1;
+  int32_t n_active = n;
   orc_detector *det = orc_detector_new(n, K);
   int64_t now = 0, processed = 0, bsp_samples = 0, version = 0, next_window = D;
   int64_t bsp_steps = 0, asp_pushes = 0, dropped = 0, windows = 0, nlog = 0;
@@ -289,10 +299,11 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
   do {                                           \
     if (st) orcf_switch(st, (to), 0);            \
     if (nlog < cap) {                            \
-      log4[4 * nlog + 0] = now;                  \
-      log4[4 * nlog + 1] = version;              \
-      log4[4 * nlog + 2] = (to);                 \
-      log4[4 * nlog + 3] = (why);                \
+      log5[5 * nlog + 0] = now;                  \
+      log5[5 * nlog + 1] = version;              \
+      log5[5 * nlog + 2] = (to);                 \
+      log5[5 * nlog + 3] = (why);                \
+      log5[5 * nlog + 4] = n_active;             \
     }                                            \
     nlog++;                                      \
     proto = (to);                                \
@@ -310,22 +321,32 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
   while (processed < W) {
     if (proto == ORC_BSP) {
       int64_t slowest = 0;
+      int32_t m = 0;
       for (int32_t j = 0; j < n; j++) {
+        if (!active[j]) continue;                      /* removed workers receive no work */
         int64_t len = STEP_LEN(j, now);
         if (len > slowest) slowest = len;
         win_busy[j] += (double)len;
         win_samples[j] += (double)B;
-        if (st) orc_synth_grad(grad_seed, j, steps[j], 0, P, g[j]);
-        ver[j] = version;
+        if (st) orc_synth_grad(grad_seed, j, steps[j], 0, P, g[m]);
+        ids[m] = j;
+        ver[m] = version;
+        m++;
       }
-      if (st) orcf_bsp_step(st, (const float *const *)g, ids, ver, n);
-      for (int32_t j = 0; j < n; j++) steps[j]++;
+      if (st) orcf_bsp_step(st, (const float *const *)g, ids, ver, m);
+      for (int32_t j = 0; j < n; j++)
+        if (active[j]) steps[j]++;
       version++;
       now += slowest;
-      processed += (int64_t)n * B;
-      bsp_samples += (int64_t)n * B;
+      processed += (int64_t)m * B;
+      bsp_samples += (int64_t)m * B;
       bsp_steps++;
       if (bsp_samples >= quota) {
+        if (n_active < n) {                            /* restore the cluster size */
+          for (int32_t j = 0; j < n; j++) { active[j] = 1; ids[j] = j; }
+          n_active = n;
+          if (st) orcf_set_members(st, ids, n);
+        }
         LOG_SWITCH(ORC_ASP, 0);
         BEGIN_ASP();
       }
@@ -336,8 +357,8 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
       now = finish[j];
       int64_t stale = 0;
       if (st) {
-        orc_synth_grad(grad_seed, j, steps[j], 0, P, g[j]);
-        orcf_asp_push(st, j, g[j], base[j], &stale);
+        orc_synth_grad(grad_seed, j, steps[j], 0, P, g[0]);
+        orcf_asp_push(st, j, g[0], base[j], &stale);
       }
       steps[j]++;
       version++;
@@ -351,7 +372,8 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
       finish[j] = now + length[j];
     }
     while (next_window <= now) {
-      int32_t clean = orc_detector_window(det, win_samples, win_busy, flag);
+      int32_t clean = orc_detector_window_masked(det, win_samples, win_busy,
+                                                 (policy == 1 && proto == ORC_BSP) ? active : NULL, flag);
       int32_t any = 0;
       for (int32_t q = 0; q < n; q++) {
         any |= flag[q];
@@ -360,13 +382,34 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
       }
       next_window += D;
       windows++;
-      if (proto == ORC_BSP && any && bsp_samples < quota) {          /* P:1421 straggler during BSP */
+      if (policy == 1) {                                             /* elastic */
+        if (proto == ORC_BSP && any && bsp_samples < quota) {
+          int32_t left = 0;
+          for (int32_t q = 0; q < n; q++) left += active[q] && !flag[q];
+          if (left >= 1) {                                           /* a non-straggler must remain */
+            int32_t m = 0;
+            for (int32_t q = 0; q < n; q++) {
+              if (flag[q]) active[q] = 0;
+              if (active[q]) ids[m++] = q;
+            }
+            n_active = m;
+            if (st) orcf_set_members(st, ids, m);
+            if (nlog < cap) {
+              log5[5 * nlog + 0] = now; log5[5 * nlog + 1] = version; log5[5 * nlog + 2] = ORC_BSP;
+              log5[5 * nlog + 3] = 3;   log5[5 * nlog + 4] = n_active;
+            }
+            nlog++;
+          }
+        }
+      } else if (policy == 2) {
+        /* no straggler policy */
+      } else if (proto == ORC_BSP && any && bsp_samples < quota) {   /* P:1421 straggler during BSP */
         LOG_SWITCH(ORC_ASP, 1);
         BEGIN_ASP();
       } else if (proto == ORC_ASP && clean && bsp_samples < quota) { /* P:1421 clean and BSP unfinished */
         LOG_SWITCH(ORC_BSP, 2);
         for (int32_t q = 0; q < n; q++) {
-          if (st) orcf_asp_push(st, q, g[q], base[q], NULL);          /* late: rejected, counted as dropped */
+          if (st) orcf_asp_push(st, q, g[0], base[q], NULL);          /* late: rejected, counted as dropped */
           steps[q]++;
           dropped++;
         }
@@ -382,6 +425,7 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
   free(g); free(steps); free(base); free(finish); free(length); free(win_samples); free(win_busy); free(flag);
   free(ver);
   free(ids);
+  free(active);
   orc_detector_free(det);
   return nlog;
 }

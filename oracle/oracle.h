@@ -55,6 +55,8 @@ typedef struct orc_d orc_d;
   void orc##SUF##_free(orc_##SUF *o);                                                                            \
   int32_t orc##SUF##_set_lr_schedule(orc_##SUF *o, const int64_t *bounds, const float *factors, int32_t nb);     \
   int32_t orc##SUF##_set_lr_policy(orc_##SUF *o, int32_t asp_rule, float weight_decay);                          \
+  int32_t orc##SUF##_set_momentum_policy(orc_##SUF *o, int32_t rule, int64_t samples_per_epoch, int64_t batch);   \
+  int32_t orc##SUF##_set_members(orc_##SUF *o, const int32_t *workers, int32_t count);                           \
   int32_t orc##SUF##_bsp_step(orc_##SUF *o, const REAL *const *grads, const int32_t *workers,                     \
                               const int64_t *versions, int32_t n_local);                                         \
   int32_t orc##SUF##_asp_push(orc_##SUF *o, int32_t worker, const REAL *grad, int64_t version, int64_t *stale);  \
@@ -100,14 +102,17 @@ void orc_detector_free(orc_detector *dt);
  * worker k has been flagged for K consecutive windows. Returns 1 if no worker was flagged for the last K windows
  * ("cluster free of stragglers", SV C15), else 0. */
 int32_t orc_detector_window(orc_detector *dt, const double *samples, const double *busy, int32_t *straggler);
+/* Same over the workers with mask[k] != 0 (elastic policy): others are not measured, not flagged, counters reset. */
+int32_t orc_detector_window_masked(orc_detector *dt, const double *samples, const double *busy, const uint8_t *mask,
+                                   int32_t *straggler);
 
 /* ---- online straggler scenario (config 4): greedy policy over the detector ----
- * st: an orcf_* state with n workers (NULL: dry run). Writes up to cap switch records {tick, version, to, reason} to
- * log4 and {bsp_steps, asp_pushes, dropped, end_tick, version, windows, n_switches} to res7. Returns n_switches. */
+ * policy 0 greedy, 1 elastic, 2 none. st: an orcf_* state with n workers (NULL: dry run).
+ * Writes up to cap records {tick, version, to, reason, members} to log5 (reason 3: elastic removal) and {bsp_steps, asp_pushes, dropped, end_tick, version, windows, n_switches} to res7. Returns n_switches. */
 int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, int64_t q_num, int64_t q_den,
                          int64_t period, int64_t jitter, uint64_t sched_seed, uint64_t grad_seed, int32_t slow_worker,
                          int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t D, int32_t K,
-                         int64_t *log4, int32_t cap, int64_t *res7);
+                         int32_t policy, int64_t *log5, int32_t cap, int64_t *res7);
 
 #ifdef __cplusplus
 }

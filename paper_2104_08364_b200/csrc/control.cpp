@@ -175,23 +175,30 @@ ss_status ss_detector_new(ss_detector **out, int32_t n, int32_t K) {
 }
 
 // S_k over the window; flagged when S_k < S - sigma (population sigma, reading C14); a straggler after K
-// consecutive flagged windows. Cluster clean after K windows without any flag (reading C15).
-ss_status ss_detector_window(ss_detector *d, const double *samples, const double *busy, int32_t *straggler,
-                             int32_t *clean_out) {
+// consecutive flagged windows. Cluster clean after K windows without any flag (reading C15). With a mask, only the
+// masked-in workers are measured (elastic policy): the others are neither in S, sigma nor flagged.
+ss_status ss_detector_window_masked(ss_detector *d, const double *samples, const double *busy, const uint8_t *mask,
+                                    int32_t *straggler, int32_t *clean_out) {
   if (!d || !samples || !busy || !straggler) return SS_E_INVAL;
   std::vector<double> s(d->n);
   double mean = 0.0;
+  int32_t m = 0;
   for (int32_t k = 0; k < d->n; ++k) {
     s[k] = busy[k] > 0.0 ? samples[k] / busy[k] : 0.0;
-    mean += s[k];
+    if (!mask || mask[k]) {
+      mean += s[k];
+      ++m;
+    }
   }
-  mean /= d->n;
+  mean = m > 0 ? mean / m : 0.0;
   double ss = 0.0;
-  for (int32_t k = 0; k < d->n; ++k) ss += (s[k] - mean) * (s[k] - mean);
-  const double thr = mean - std::sqrt(ss / d->n);
+  for (int32_t k = 0; k < d->n; ++k)
+    if (!mask || mask[k]) ss += (s[k] - mean) * (s[k] - mean);
+  const double thr = mean - std::sqrt(m > 0 ? ss / m : 0.0);
   bool any = false;
   for (int32_t k = 0; k < d->n; ++k) {
-    const bool f = s[k] < thr;
+    const bool in = !mask || mask[k];
+    const bool f = in && s[k] < thr;
     d->run[k] = f ? d->run[k] + 1 : 0;
     straggler[k] = d->run[k] >= d->K;
     any = any || f;
@@ -199,6 +206,11 @@ ss_status ss_detector_window(ss_detector *d, const double *samples, const double
   d->clean = any ? 0 : d->clean + 1;
   if (clean_out) *clean_out = d->clean >= d->K;
   return SS_OK;
+}
+
+ss_status ss_detector_window(ss_detector *d, const double *samples, const double *busy, int32_t *straggler,
+                             int32_t *clean_out) {
+  return ss_detector_window_masked(d, samples, busy, nullptr, straggler, clean_out);
 }
 
 void ss_detector_free(ss_detector *d) { delete d; }

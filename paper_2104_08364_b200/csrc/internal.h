@@ -57,6 +57,7 @@ struct AspEvent {
   const float *src;   // push: gradient slice
   float *dst;         // pull: snapshot destination slice (nullptr: no data)
   float lr;           // push: eta_ASP at the push's version
+  float mu;           // push: momentum for this push (constant unless a post-switch momentum policy is set)
   int32_t kind;       // 0 push, 1 pull
 };
 struct AspArgs {
@@ -66,7 +67,6 @@ struct AspArgs {
   int *flag;
   int64_t count;
   int32_t n_ev;
-  float mu;
   float lam;
   PeerSync sync;
 };

@@ -250,12 +250,13 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
   if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const float mu = a.mu, lam = a.lam;
+  const float lam = a.lam;
   bool bad = false;
   int first_push = 0;
   while (first_push < a.n_ev && a.ev[first_push].kind != 0) ++first_push;
 
-  auto apply1 = [&](float g, float &w, float &v, float neg_eta) {
+  // per-push momentum: the post-switch momentum policy may vary it push by push
+  auto apply1 = [&](float g, float &w, float &v, float neg_eta, float mu) {
     if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
     v = __fmaf_rn(mu, v, g);
     w = __fmaf_rn(neg_eta, v, w);
@@ -290,14 +291,14 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
             for (int u = 0; u < kU2; ++u)
               if (ok[u]) gn[u] = ld4(a.ev[next].src + 4 * (q0 + u * stride));
           }
-          const float neg_eta = -a.ev[e].lr;
+          const float neg_eta = -a.ev[e].lr, mu_e = a.ev[e].mu;
 #pragma unroll
           for (int u = 0; u < kU2; ++u) {
             if (!ok[u]) continue;
-            apply1(gc[u].x, wv[u].x, vv[u].x, neg_eta);
-            apply1(gc[u].y, wv[u].y, vv[u].y, neg_eta);
-            apply1(gc[u].z, wv[u].z, vv[u].z, neg_eta);
-            apply1(gc[u].w, wv[u].w, vv[u].w, neg_eta);
+            apply1(gc[u].x, wv[u].x, vv[u].x, neg_eta, mu_e);
+            apply1(gc[u].y, wv[u].y, vv[u].y, neg_eta, mu_e);
+            apply1(gc[u].z, wv[u].z, vv[u].z, neg_eta, mu_e);
+            apply1(gc[u].w, wv[u].w, vv[u].w, neg_eta, mu_e);
           }
         } else if (a.ev[e].dst != nullptr) {
           float *dst = a.ev[e].dst;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
     if (i < a.count) {
       float w = a.w[i], v = a.v[i];
       for (int e = 0; e < a.n_ev; ++e) {
-        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr);
+        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr, a.ev[e].mu);
         else if (a.ev[e].dst) a.ev[e].dst[i] = w;
       }
       bad |= nonfinite(w) | nonfinite(v);
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
     for (int64_t i = tid; i < a.count; i += stride) {
       float w = a.w[i], v = a.v[i];
       for (int e = 0; e < a.n_ev; ++e) {
-        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr);
+        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr, a.ev[e].mu);
         else if (a.ev[e].dst) a.ev[e].dst[i] = w;
       }
       bad |= nonfinite(w) | nonfinite(v);
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int push_ev[kMaxEvents];
   __shared__ int n_push_s;
-  const float mu = a.mu, lam = a.lam;
+  const float lam = a.lam;
   if (threadIdx.x == 0) {
     int np = 0;
     for (int e = 0; e < a.n_ev; ++e)
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
       if (a.ev[e].kind == 0) {
         const int s = (int)(it % kTmaStages);
         mbar_wait(&full[s], (uint32_t)((it / kTmaStages) & 1));
-        const float neg_eta = -a.ev[e].lr;
+        const float neg_eta = -a.ev[e].lr, mu = a.ev[e].mu;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (!ok[u]) continue;
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
         if (a.ev[e].kind == 0) {
           float gg = a.ev[e].src[i];
           if (lam != 0.0f) gg = __fmaf_rn(lam, w, gg);
-          v = __fmaf_rn(mu, v, gg);
+          v = __fmaf_rn(a.ev[e].mu, v, gg);
           w = __fmaf_rn(-a.ev[e].lr, v, w);
         } else if (a.ev[e].dst) {
           a.ev[e].dst[i] = w;

@@ -32,6 +32,7 @@ struct Ev {
   float *dst;           // pull: device destination (full length) on the hosting rank, else nullptr
   float *host_dst;      // pull into host memory: D2H from dst after the window
   float lr;             // push: eta_ASP at the push's (pre-increment) version
+  float mu;             // push: momentum (post-switch momentum policy)
   bool data;            // pull: moves parameters (false: version-only pull, G = 1)
 };
 
@@ -57,6 +58,11 @@ struct ss_ctx {
   std::vector<int64_t> off;
   float eta = 0.f, mu = 0.f, lam = 0.f;
   int32_t asp_rule = 0;
+  int32_t mom_rule = 0;                // post-switch momentum policy: 0 same mu, 1 zero, 2 1/n, 3 2^i/n, 4 i/n
+  int64_t mom_epoch_samples = 1, mom_batch = 1;
+  int64_t asp_since = 0;               // version at which the last switch to ASP took effect
+  std::vector<uint8_t> member;         // BSP barrier set (elastic policy); all workers by default
+  int32_t n_members = 0;
   std::vector<int64_t> bounds;
   std::vector<float> factors;
   // distribution
@@ -169,11 +175,24 @@ float lr_at(const ss_ctx *c, int64_t ver, int32_t proto) {
   for (size_t i = 0; i < c->bounds.size(); ++i)
     if (c->bounds[i] <= ver) f = (double)c->factors[i];
   double scale;
-  if (proto == SS_BSP) scale = (double)c->n;
+  if (proto == SS_BSP) scale = (double)c->n_members;   // linear scaling over the BSP workers
   else if (c->asp_rule == 0) scale = 1.0 / std::sqrt((double)c->n);
   else if (c->asp_rule == 1) scale = 1.0 / (double)c->n;
   else scale = 1.0;
   return (float)((double)c->eta * f * scale);
+}
+
+// Momentum of an ASP push (P:1458 / P:618-619): (i) 0, (ii) 1/n, (iii) 2^i/n, (iv) i/n with i = completed epochs since
+// the switch to ASP (each push is B samples); ramps stop at the BSP value; rule 0 keeps the BSP momentum.
+float asp_momentum(const ss_ctx *c, int64_t ver) {
+  if (c->mom_rule == 0) return c->mu;
+  const int64_t i = (ver - c->asp_since) * c->mom_batch / c->mom_epoch_samples;
+  double m;
+  if (c->mom_rule == 1) m = 0.0;
+  else if (c->mom_rule == 2) m = 1.0 / (double)c->n;
+  else if (c->mom_rule == 3) m = std::ldexp(1.0, (int)std::min<int64_t>(i, 1000)) / (double)c->n;
+  else m = (double)i / (double)c->n;
+  return (float)std::min(m, (double)c->mu);
 }
 
 void record(ss_ctx *c, int64_t worker, int64_t b, int64_t st) {
@@ -405,6 +424,7 @@ ss_status flush_fused(ss_ctx *c) {
     if (e.kind == 0) {
       x.src = host_of(c, e.worker) == me ? e.src + lo : c->inbox + (int64_t)k * c->reg_len;
       x.lr = e.lr;
+      x.mu = e.mu;
       vec = vec && aligned16(x.src);
       ++n_push;
     } else {
@@ -420,7 +440,6 @@ ss_status flush_fused(ss_ctx *c) {
   a.v = c->v;
   a.flag = c->flag;
   a.count = cnt;
-  a.mu = c->mu;
   a.lam = c->lam;
   a.sync = peer_sync(c, epA, epB, true);
   Timed t;
@@ -496,6 +515,7 @@ ss_status flush(ss_ctx *c) {
         if (e.kind == 0) {
           x.src = (c->world == 1 || host_of(c, e.worker) == me) ? e.src + lo : c->rslot[k];
           x.lr = e.lr;
+          x.mu = e.mu;
           vec = vec && aligned16(x.src);
         } else {
           if (!e.data) continue;  // version-only pull: no data
@@ -509,7 +529,6 @@ ss_status flush(ss_ctx *c) {
       a.v = c->v;
       a.flag = c->flag;
       a.count = cnt;
-      a.mu = c->mu;
       a.lam = c->lam;
       Timed t;
       timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
@@ -549,6 +568,8 @@ ss_status maybe_switch(ss_ctx *c) {
       c->proto = c->pending_proto;
       if (c->proto == SS_BSP)
         for (auto &b : c->base) b = c->version;
+      else
+        c->asp_since = c->version;
     }
   }
   return SS_OK;
@@ -613,6 +634,8 @@ ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n
   c->off.resize(n_shards + 1);
   for (int32_t s = 0; s <= n_shards; ++s) c->off[s] = std::min<int64_t>((int64_t)s * c->pad, n_params);
   c->base.assign(n_workers, 0);
+  c->member.assign(n_workers, 1);
+  c->n_members = n_workers;
   c->L = ss::make_layout(n_params, n_shards, n_workers, 0, 1);
   c->reg_len = c->L.reg_len;
   c->real_lo = c->L.real_lo;
@@ -717,6 +740,29 @@ ss_status ss_set_lr_policy(ss_ctx *c, int32_t asp_rule, float weight_decay) {
   return SS_OK;
 }
 
+ss_status ss_set_momentum_policy(ss_ctx *c, int32_t rule, int64_t samples_per_epoch, int64_t batch) {
+  SS_TRY(check_live(c));
+  if (rule < 0 || rule > 4 || samples_per_epoch < 1 || batch < 1) return fail(c, SS_E_INVAL, "bad momentum policy");
+  c->mom_rule = rule;
+  c->mom_epoch_samples = samples_per_epoch;
+  c->mom_batch = batch;
+  return SS_OK;
+}
+
+ss_status ss_set_members(ss_ctx *c, const int32_t *workers, int32_t count) {
+  SS_TRY(check_live(c));
+  if (count < 1 || count > c->n || !workers) return fail(c, SS_E_INVAL, "member set must hold 1..n workers");
+  std::vector<uint8_t> m(c->n, 0);
+  for (int32_t i = 0; i < count; ++i) {
+    if (workers[i] < 0 || workers[i] >= c->n || m[workers[i]])
+      return fail(c, SS_E_INVAL, "bad or duplicate member %d", workers[i]);
+    m[workers[i]] = 1;
+  }
+  c->member = m;
+  c->n_members = count;
+  return SS_OK;
+}
+
 ss_status ss_current_lr(ss_ctx *c, int32_t proto, float *lr_out) {
   if (!c || !lr_out || (proto != SS_BSP && proto != SS_ASP)) return SS_E_INVAL;
   *lr_out = lr_at(c, c->version, proto);
@@ -729,14 +775,16 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   if (!grads || !workers || !versions || n_local < 0) return fail(c, SS_E_INVAL, "null argument");
   SS_TRY(maybe_switch(c));
   if (c->proto != SS_BSP) return fail(c, SS_E_STATE, "ss_bsp_step under ASP");
-  // barrier: exactly the expected workers (all n; multi-GPU: this rank's hosted workers), each once
+  // barrier: exactly the expected workers (the BSP members; multi-GPU: this rank's hosted members), each once
+  // (elastic policy S:246-254)
   std::vector<const float *> by(c->n, nullptr);
   int32_t expected = 0;
-  for (int32_t j = 0; j < c->n; ++j) expected += host_of(c, j) == c->rank;
+  for (int32_t j = 0; j < c->n; ++j) expected += host_of(c, j) == c->rank && c->member[j];
   for (int32_t i = 0; i < n_local; ++i) {
     const int32_t j = workers[i];
     if (j < 0 || j >= c->n) return fail(c, SS_E_INVAL, "worker %d out of range", j);
     if (host_of(c, j) != c->rank) return fail(c, SS_E_PROTOCOL, "worker %d is not hosted on rank %d", j, c->rank);
+    if (!c->member[j]) return fail(c, SS_E_PROTOCOL, "worker %d is not a BSP member", j);
     if (by[j] || !grads[i]) return fail(c, SS_E_PROTOCOL, "duplicate or null gradient for worker %d", j);
     by[j] = grads[i];
   }
@@ -752,8 +800,10 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   std::memset(&a, 0, sizeof a);
   bool vec = true;
   int32_t k = 0;
+  std::vector<int32_t> ids;             // hosted members, ascending
   for (int32_t j = 0; j < c->n; ++j) {  // ascending worker order (reading C12)
     if (!by[j]) continue;
+    ids.push_back(j);
     const float *g = nullptr;
     SS_TRY(resolve_src(c, by[j], &g));
     a.g[k++] = g;
@@ -761,7 +811,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   }
   const float eta_t = lr_at(c, c->version, SS_BSP);  // pre-increment version (reading C9)
   a.flag = c->flag;
-  a.divisor = (float)c->n;
+  a.divisor = (float)c->n_members;
   a.mu = c->mu;
   a.neg_eta = -eta_t;
   a.lam = c->lam;
@@ -780,7 +830,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     // w and v, and stores the new w slice into every rank's replica; one flag barrier closes the step.
     const bool presum = c->fused_mode == 2;
     SS_TRY(ensure_fused(c, presum ? c->world : c->n));
-    SS_TRY(ensure_dist_buffers(c));
+    SS_TRY(ensure_dist_buffers(c));   // (sum_buf, rs_buf: NCCL mode only; allocated once)
     const uint32_t epA = ++c->epoch, epB = ++c->epoch;
     const int32_t me = c->rank;
     const int64_t lo = c->real_lo[me], cnt = c->real_hi[me] - lo;
@@ -804,7 +854,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       SS_CUDA(c, ss::launch_scatter_sum(sa, c->stream));
       timed_end(c, &t);
     } else {
-      for (int32_t i = 0; i < k; ++i) src.push_back({a.g[i], c->first_hosted + i});
+      for (int32_t i = 0; i < k; ++i) src.push_back({a.g[i], ids[i]});
       SS_TRY(launch_scatter(c, src, epA));
     }
     const float *hosted_g[ss::kMaxWorkers];
@@ -814,9 +864,12 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       for (int32_t q = 0; q < c->world; ++q) a.g[q] = c->inbox + (int64_t)q * c->reg_len;
       a.n_in = c->world;
     } else {
-      for (int32_t j = 0; j < c->n; ++j)
-        a.g[j] = host_of(c, j) == me ? hosted_g[j - c->first_hosted] + lo : c->inbox + (int64_t)j * c->reg_len;
-      a.n_in = c->n;
+      int32_t ni = 0, h = 0;
+      for (int32_t j = 0; j < c->n; ++j) {   // the members' slices, ascending worker order
+        if (!c->member[j]) continue;
+        a.g[ni++] = host_of(c, j) == me ? hosted_g[h++] + lo : c->inbox + (int64_t)j * c->reg_len;
+      }
+      a.n_in = ni;
     }
     a.w = c->w + lo;
     a.v = c->v;
@@ -862,7 +915,8 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
                              c->stream));
   }
   c->stage_used = 0;
-  for (int32_t j = 0; j < c->n; ++j) record(c, j, c->version, 0);  // n staleness-0 records
+  for (int32_t j = 0; j < c->n; ++j)
+    if (c->member[j]) record(c, j, c->version, 0);  // one staleness-0 record per BSP member
   c->version += 1;
   for (auto &b : c->base) b = c->version;
   return SS_OK;
@@ -885,6 +939,7 @@ ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t vers
   e.worker = worker;
   if (mine) SS_TRY(resolve_src(c, grad, &e.src));
   e.lr = lr_at(c, c->version, SS_ASP);
+  e.mu = asp_momentum(c, c->version);
   const int64_t st = c->version - version;
   record(c, worker, version, st);
   c->version += 1;

@@ -39,7 +39,7 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
   const int32_t n = sc->n_workers;
   if (n < 1 || n > ss::kMaxWorkers || sc->batch < 1 || sc->total_samples < 1 || sc->quota_den < 1 ||
       sc->quota_num < 0 || sc->quota_num > sc->quota_den || sc->jitter < 0 || sc->period <= sc->jitter ||
-      sc->window_ticks < 1 || sc->K < 1 || sc->slow_factor < 1)
+      sc->window_ticks < 1 || sc->K < 1 || sc->slow_factor < 1 || sc->policy < 0 || sc->policy > 2)
     return SS_E_INVAL;
 
   ss::CtxInfo info{};
@@ -83,6 +83,9 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
   std::vector<int32_t> strag(n, 0);
   int64_t t = 0, done = 0, bsp_done = 0, version = 0, win_end = D, ring = 0;
   int32_t proto = SS_BSP, n_log = 0;
+  // BSP barrier set (elastic policy): removed workers stop receiving work until the quota is met
+  std::vector<uint8_t> mem(n, 1);
+  int32_t n_mem = n;
   ss_scenario_result r{};
   ss_detector *dt = nullptr;
   if (ss_detector_new(&dt, n, sc->K) != SS_OK) return SS_E_INVAL;
@@ -113,7 +116,7 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
       ss_status s = ss_switch(ctx, to, 0);
       if (s != SS_OK) return s;
     }
-    if (n_log < cap) log[n_log] = ss_switch_event{t, version, to, reason};
+    if (n_log < cap) log[n_log] = ss_switch_event{t, version, to, reason, n_mem};
     ++n_log;
     proto = to;
     return SS_OK;
@@ -137,13 +140,25 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
     return SS_OK;
   };
 
+  auto set_members = [&]() -> ss_status {
+    if (!ctx) return SS_OK;
+    std::vector<int32_t> ids;
+    for (int32_t j = 0; j < n; ++j)
+      if (mem[j]) ids.push_back(j);
+    return ss_set_members(ctx, ids.data(), (int32_t)ids.size());
+  };
+  auto log_event = [&](int32_t to, int32_t reason) {
+    if (n_log < cap) log[n_log] = ss_switch_event{t, version, to, reason, n_mem};
+    ++n_log;
+  };
+
   while (done < W) {
     if (proto == SS_BSP) {
       std::vector<const float *> g;
       std::vector<int32_t> ws;
       std::vector<int64_t> vs;
       for (int32_t j = 0; j < n; ++j) {
-        if (!hosted(j)) continue;
+        if (!mem[j] || !hosted(j)) continue;
         ss_status s = gen(j, ctx ? buf.bsp[j] : nullptr);
         if (s != SS_OK) return s;
         g.push_back(ctx ? buf.bsp[j] : nullptr);
@@ -156,18 +171,26 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
       }
       int64_t mx = 0;
       for (int32_t j = 0; j < n; ++j) {
+        if (!mem[j]) continue;
         const int64_t dj = gap(j, t);
         acc_b[j] += (double)dj;   // busy time excludes the barrier wait (reading C14)
         acc_s[j] += (double)B;
         mx = std::max(mx, dj);
       }
-      for (int32_t j = 0; j < n; ++j) c[j] += 1;
+      for (int32_t j = 0; j < n; ++j)
+        if (mem[j]) c[j] += 1;
       version += 1;
       t += mx;
-      done += (int64_t)n * B;
-      bsp_done += (int64_t)n * B;
+      done += (int64_t)n_mem * B;
+      bsp_done += (int64_t)n_mem * B;
       r.bsp_steps += 1;
-      if (bsp_done >= quota) {  // timing policy: the BSP share is done, ASP for the rest
+      if (bsp_done >= quota) {  // timing policy: the BSP share is done; restore every worker, ASP for the rest
+        if (n_mem < n) {
+          std::fill(mem.begin(), mem.end(), 1);
+          n_mem = n;
+          ss_status s = set_members();
+          if (s != SS_OK) return s;
+        }
         ss_status s = do_switch(SS_ASP, 0);
         if (s == SS_OK) s = start_asp();
         if (s != SS_OK) return s;
@@ -197,31 +220,46 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
       dur[j] = gap(j, t);
       nxt[j] = t + dur[j];
     }
-    while (t >= win_end) {  // detection windows (win_end - D, win_end] closed by time t
+    while (t >= win_end) {  // detection windows closed by time t (the current event is counted in the closing one)
       int32_t clean = 0;
-      ss_detector_window(dt, acc_s.data(), acc_b.data(), strag.data(), &clean);
+      const bool masked = sc->policy == 1 && proto == SS_BSP;
+      ss_detector_window_masked(dt, acc_s.data(), acc_b.data(), masked ? mem.data() : nullptr, strag.data(),
+                                &clean);
       std::fill(acc_s.begin(), acc_s.end(), 0.0);
       std::fill(acc_b.begin(), acc_b.end(), 0.0);
       win_end += D;
       r.windows += 1;
       int32_t any = 0;
       for (int32_t q = 0; q < n; ++q) any |= strag[q];
-      const int32_t dec = ss_greedy_decision(proto, any, clean, bsp_done, quota);
-      if (dec == SS_ASP) {
-        ss_status s = do_switch(SS_ASP, 1);
-        if (s == SS_OK) s = start_asp();
-        if (s != SS_OK) return s;
-      } else if (dec == SS_BSP) {
-        ss_status s = do_switch(SS_BSP, 2);
-        if (s != SS_OK) return s;
-        for (int32_t q = 0; q < n; ++q) {  // every worker's in-flight gradient arrives late and is dropped
-          if (ctx) {
-            int64_t st = 0;
-            s = ss_asp_push(ctx, q, hosted(q) ? buf.asp[0] : nullptr, base[q], &st);
-            if (s != SS_E_STATE) return s == SS_OK ? SS_E_STATE : s;
+      if (sc->policy == 0) {  // greedy
+        const int32_t dec = ss_greedy_decision(proto, any, clean, bsp_done, quota);
+        if (dec == SS_ASP) {
+          ss_status s = do_switch(SS_ASP, 1);
+          if (s == SS_OK) s = start_asp();
+          if (s != SS_OK) return s;
+        } else if (dec == SS_BSP) {
+          ss_status s = do_switch(SS_BSP, 2);
+          if (s != SS_OK) return s;
+          for (int32_t q = 0; q < n; ++q) {  // every worker's in-flight gradient arrives late and is dropped
+            if (ctx) {
+              int64_t st = 0;
+              s = ss_asp_push(ctx, q, hosted(q) ? buf.asp[0] : nullptr, base[q], &st);
+              if (s != SS_E_STATE) return s == SS_OK ? SS_E_STATE : s;
+            }
+            c[q] += 1;
+            r.dropped += 1;
           }
-          c[q] += 1;
-          r.dropped += 1;
+        }
+      } else if (sc->policy == 1 && proto == SS_BSP && any && bsp_done < quota) {  // elastic
+        int32_t keep = 0;
+        for (int32_t q = 0; q < n; ++q) keep += mem[q] && !strag[q];
+        if (keep >= 1) {  // at least one non-straggler stays
+          for (int32_t q = 0; q < n; ++q)
+            if (strag[q]) mem[q] = 0;
+          n_mem = keep;
+          ss_status s = set_members();
+          if (s != SS_OK) return s;
+          log_event(SS_BSP, 3);
         }
       }
     }

@@ -31,7 +31,7 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
            "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer",
-           "ss_scenario_run"]
+           "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked"]
 
 
 class SSError(RuntimeError):
@@ -51,12 +51,13 @@ class ss_scenario(ctypes.Structure):
                 ("quota_num", ctypes.c_int64), ("quota_den", ctypes.c_int64), ("period", ctypes.c_int64),
                 ("jitter", ctypes.c_int64), ("sched_seed", ctypes.c_uint64), ("grad_seed", ctypes.c_uint64),
                 ("slow_worker", ctypes.c_int32), ("slow_factor", ctypes.c_int64), ("slow_t0", ctypes.c_int64),
-                ("slow_t1", ctypes.c_int64), ("window_ticks", ctypes.c_int64), ("K", ctypes.c_int32)]
+                ("slow_t1", ctypes.c_int64), ("window_ticks", ctypes.c_int64), ("K", ctypes.c_int32),
+                ("policy", ctypes.c_int32)]
 
 
 class ss_switch_event(ctypes.Structure):
     _fields_ = [("tick", ctypes.c_int64), ("version", ctypes.c_int64), ("to_protocol", ctypes.c_int32),
-                ("reason", ctypes.c_int32)]
+                ("reason", ctypes.c_int32), ("members", ctypes.c_int32)]
 
 
 class ss_scenario_result(ctypes.Structure):
@@ -85,6 +86,9 @@ def _load():
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
         "ss_set_lr_policy": [p, i32, f32],
+        "ss_set_momentum_policy": [p, i32, i64, i64],
+        "ss_set_members": [p, p, i32],
+        "ss_detector_window_masked": [p, p, p, p, p, p],
         "ss_current_lr": [p, i32, p],
         "ss_bsp_step": [p, p, p, p, i32],
         "ss_asp_push": [p, i32, p, i64, p],
@@ -344,7 +348,7 @@ def ss_scenario_run(ctx, sc: dict, cap: int = 256):
     out = ss_scenario_result()
     s = lib.ss_scenario_run(ctx, ctypes.byref(c), ctypes.byref(out), ctypes.cast(log, ctypes.c_void_p), cap)
     res = {k: getattr(out, k) for k, _ in ss_scenario_result._fields_}
-    entries = [(e.tick, e.version, e.to_protocol, e.reason) for e in log[:min(out.n_switches, cap)]]
+    entries = [(e.tick, e.version, e.to_protocol, e.reason, e.members) for e in log[:min(out.n_switches, cap)]]
     return s, entries, res
 
 
@@ -356,13 +360,15 @@ class Detector:
         ss_check(lib.ss_detector_new(ctypes.byref(h), n, K))
         self._h, self.n = h.value, n
 
-    def window(self, samples, busy):
+    def window(self, samples, busy, mask=None):
         s = _a(samples, np.float64)
         b = _a(busy, np.float64)
+        m = _a(mask, np.uint8) if mask is not None else None
         flag = np.zeros(self.n, dtype=np.int32)
         clean = ctypes.c_int32()
-        ss_check(lib.ss_detector_window(self._h, s.ctypes.data, b.ctypes.data, flag.ctypes.data,
-                                        ctypes.byref(clean)))
+        ss_check(lib.ss_detector_window_masked(self._h, s.ctypes.data, b.ctypes.data,
+                                               m.ctypes.data if m is not None else None, flag.ctypes.data,
+                                               ctypes.byref(clean)))
         return flag.astype(bool), bool(clean.value)
 
     def __del__(self):
@@ -421,6 +427,13 @@ class SyncSwitch:
 
     def set_lr_policy(self, asp_rule: int, weight_decay: float = 0.0):
         return self._chk(ss_set_lr_policy(self.ctx, asp_rule, weight_decay))
+
+    def set_members(self, workers):
+        w = _a(workers, np.int32)
+        return self._chk(lib.ss_set_members(self.ctx, w.ctypes.data, w.size))
+
+    def set_momentum_policy(self, rule: int, samples_per_epoch: int = 1, batch: int = 1):
+        return self._chk(lib.ss_set_momentum_policy(self.ctx, rule, samples_per_epoch, batch))
 
     def current_lr(self, protocol: int) -> float:
         return ss_current_lr(self.ctx, protocol)

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--pushes", type=int, default=60)
     ap.add_argument("--bsp2", type=int, default=2)
     ap.add_argument("--fused", type=int, default=-1)
+    ap.add_argument("--drop", type=int, default=-1, help="elastic: worker left out of --bsp-drop BSP steps")
+    ap.add_argument("--bsp-drop", type=int, default=0)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -67,6 +69,14 @@ def main():
     for _ in range(a.bsp1):
         gs = {j: grad(j) for j in range(n)}
         g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
+    if a.drop >= 0:
+        members = [j for j in range(n) if j != a.drop]
+        g.set_members(members)
+        mine = [j for j in hosted if j in members]
+        for _ in range(a.bsp_drop):
+            gs = {j: grad(j) for j in members}
+            g.bsp_step([gs[j] for j in mine], mine, [g.version] * len(mine))
+        g.set_members(list(range(n)))
     g.switch(ss.SS_ASP, 0)
     kind, worker, _ = ss.ss_schedule(n, [1000 + 100 * j for j in range(n)], a.pushes, jitter=100, seed=7)[1]
     base, stale, snaps = {}, [], []

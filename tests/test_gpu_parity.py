@@ -409,3 +409,39 @@ def test_config1_toy_end_to_end(ss, orc):
     assert close_c13(g.params(), o.params())
     assert np.mean(losses[-10:]) < 0.5 * losses[0]       # it trains
     g.close()
+
+
+@pytest.mark.parametrize("rule", [1, 2, 3, 4])
+def test_momentum_policies_bit_exact(ss, orc, rule):
+    """Post-switch momentum variants: per-push momentum in the replay kernel, bit-exact with the oracle."""
+    n, S, P = 4, 2, 5003
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for x in (g, o):
+        x.set_momentum_policy(rule, samples_per_epoch=3 * 64, batch=64)
+    keep = []
+    for step in range(2):
+        d = [dev_synth(ss, j, step, P) for j in range(n)]
+        keep += d
+        g.bsp_step(d)
+        assert o.bsp_step([host_synth(orc, j, step, P) for j in range(n)]) == 0
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    g.set_window(5)
+    kind, worker, _ = orc.schedule(n, [1000, 1200, 1500, 1700], 30, jitter=100, seed=5)
+    base_g, base_o, cnt = {}, {}, collections.Counter()
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            base_g[j] = g.pull(j)
+            base_o[j] = o.pull(j, False)[2]
+        else:
+            k = 2 + cnt[j]
+            cnt[j] += 1
+            d = dev_synth(ss, j, k, P)
+            keep.append(d)
+            assert g.asp_push(j, d, base_g[j]) == o.asp_push(j, host_synth(orc, j, k, P), base_o[j])[1]
+    g.sync()
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    g.close()

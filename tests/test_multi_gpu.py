@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SEED = 20241018
 
 
-def oracle_run(orc, P, n, S, bsp1, pushes, bsp2):
+def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0):
     w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
     o.set_lr_schedule([bsp1 + 10], [0.5])
@@ -33,6 +33,12 @@ def oracle_run(orc, P, n, S, bsp1, pushes, bsp2):
 
     for _ in range(bsp1):
         assert o.bsp_step([grad(j) for j in range(n)]) == 0
+    if drop >= 0:                                        # elastic: BSP without worker `drop`
+        members = [j for j in range(n) if j != drop]
+        o.set_members(members)
+        for _ in range(bsp_drop):
+            assert o.bsp_step([grad(j) for j in members], workers=members) == 0
+        o.set_members(list(range(n)))
     o.switch(orc.ASP, 0)
     kind, worker, _ = orc.schedule(n, [1000 + 100 * j for j in range(n)], pushes, jitter=100, seed=7)
     base, stale, snaps = {}, [], {j: [] for j in range(n)}
@@ -66,19 +72,21 @@ def close_c13(x, y, rel=1e-5):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", ["asp_only", "switched", "switched_fused", "switched_presum"])
+@pytest.mark.parametrize("case", ["asp_only", "switched", "switched_fused", "switched_presum", "elastic_fused",
+                                  "elastic_nccl"])
 def test_multi_gpu_parity(orc, world, case):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     P, n, S, win = 100003, 8, 8, 7
     bsp1, pushes, bsp2 = (0, 80, 0) if case == "asp_only" else (3, 60, 2)
-    fused = {"switched_fused": 1, "switched_presum": 2}.get(case, 0)
+    fused = {"switched_fused": 1, "switched_presum": 2, "elastic_fused": 1}.get(case, 0)
+    drop, bsp_drop = (1, 3) if case.startswith("elastic") else (-1, 0)
     with tempfile.TemporaryDirectory() as tmp:
         launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", win, "--bsp1", bsp1, "--pushes", pushes,
-                       "--bsp2", bsp2, "--fused", fused], tmp)
+                       "--bsp2", bsp2, "--fused", fused, "--drop", drop, "--bsp-drop", bsp_drop], tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
-    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2)
-    exact = case in ("asp_only", "switched_fused")   # NCCL / pre-summed BSP: other summation orders (C13)
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop, bsp_drop)
+    exact = case in ("asp_only", "switched_fused", "elastic_fused")   # NCCL / pre-summed: other sum orders (C13)
     ow, ov = o.params(), o.velocity()
     for r in res:
         # protocol integers: exact on every rank

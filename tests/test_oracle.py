@@ -443,3 +443,52 @@ def test_detector_arithmetic(orc):
     assert dt2.window([100, 100, 100, 60], [1, 1, 1, 1])[0][3]
     # throughput is samples / busy time: 4x the busy time for the same samples is a 4x slower worker
     assert list(dt2.window([10, 10, 10, 10], [1, 1, 1, 4])[0]) == [False, False, False, True]
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# post-switch momentum variants
+def _mu_sequence(orc, rule, n=8, mu=0.9, pushes=12, epoch_pushes=2):
+    # P = 1; one BSP step with unit gradients makes v = 1; after the switch every push has gradient 1, so
+    # v_{k+1} = mu_k * v_k + 1 reveals mu_k = (v_{k+1} - 1) / v_k
+    o = orc.Oracle([0.0], 1, n, 0.01, mu, dtype=np.float64)
+    assert o.set_momentum_policy(rule, samples_per_epoch=epoch_pushes * 128, batch=128) == 0
+    assert o.bsp_step([[1.0]] * n) == 0 and o.velocity()[0] == 1.0
+    o.switch(ASP, 0)
+    mus = []
+    for k in range(pushes):
+        v = o.velocity()[0]
+        rc, _ = o.asp_push(k % n, [1.0], o.version)
+        assert rc == 0
+        mus.append((o.velocity()[0] - 1.0) / v)
+    return mus
+
+
+def test_momentum_variants_sequences(orc):
+    f32 = lambda x: float(np.float32(x))  # noqa: E731  (mu travels as fp32)
+    n, mu = 8, f32(0.9)
+    want = {
+        0: [mu] * 12,                                                  # same momentum (the paper's choice)
+        1: [0.0] * 12,                                                 # (i) 0
+        2: [1 / n] * 12,                                               # (ii) 1/n
+        3: [1 / 8, 1 / 8, 2 / 8, 2 / 8, 4 / 8, 4 / 8] + [mu] * 6,       # (iii) 2^i/n, capped at the BSP value
+        4: [0, 0, 1 / 8, 1 / 8, 2 / 8, 2 / 8, 3 / 8, 3 / 8, 4 / 8, 4 / 8, 5 / 8, 5 / 8],   # (iv) i/n
+    }
+    for rule, seq in want.items():
+        got = _mu_sequence(orc, rule)
+        np.testing.assert_allclose(got, seq, rtol=1e-12, atol=1e-15, err_msg=f"rule {rule}")
+    # the i/n ramp stops at the BSP momentum too
+    assert _mu_sequence(orc, 4, pushes=40)[-1] == pytest.approx(mu, rel=1e-12)
+
+
+def test_momentum_zero_is_plain_sgd_after_switch(orc):
+    rng = np.random.default_rng(21)
+    w0 = rng.standard_normal(64).astype(np.float32)
+    g = rng.standard_normal(64).astype(np.float32)
+    o = orc.Oracle(w0, 2, 1, 0.125, 0.9)
+    o.set_momentum_policy(1)
+    o.bsp_step([g])                      # builds up v
+    o.switch(ASP, 0)
+    w1 = o.params()
+    assert o.asp_push(0, g, o.version)[0] == 0
+    assert np.array_equal(o.velocity(), g)                     # mu = 0: v' = g exactly
+    assert np.array_equal(o.params(), (w1.astype(np.float64) - 0.125 * g.astype(np.float64)).astype(np.float32))

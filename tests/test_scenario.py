@@ -9,7 +9,7 @@ import pytest
 
 BASE = dict(n_workers=8, batch=128, total_samples=64000 * 128, quota_num=1, quota_den=4, period=1000, jitter=0,
             sched_seed=7, grad_seed=20241018, slow_worker=7, slow_factor=4, slow_t0=20000, slow_t1=120000,
-            window_ticks=10000, K=3)
+            window_ticks=10000, K=3, policy=0)
 
 
 @pytest.fixture(scope="module")
@@ -29,6 +29,11 @@ CASES = [
          slow_t1=50000, K=2, window_ticks=5000),
     dict(BASE, quota_num=0, quota_den=1),
     dict(BASE, quota_num=1, quota_den=1, total_samples=2000 * 128 * 8),
+    dict(BASE, policy=1),
+    dict(BASE, policy=1, jitter=100),
+    dict(BASE, policy=1, n_workers=4, slow_worker=2, total_samples=8000 * 128, quota_num=1, quota_den=2, K=2,
+         window_ticks=5000, slow_t0=0, slow_t1=50000),
+    dict(BASE, policy=2),
 ]
 
 
@@ -46,7 +51,7 @@ def test_no_straggler_preserves_table1(orc, split):
     log, res = orc.scenario(sc)
     bsp, asp, _ = orc.table1(64000 * 128, 128, 8, split[0], 100, [])
     assert (res["bsp_steps"], res["asp_pushes"]) == (bsp, asp)
-    assert log == [(bsp * 1000, bsp, 1, 0)]          # switch to ASP once, at version = BSP steps
+    assert log == [(bsp * 1000, bsp, 1, 0, 8)]       # switch to ASP once, at version = BSP steps
     assert res["dropped"] == 0 and res["version"] == bsp + asp
 
 
@@ -57,12 +62,52 @@ def test_greedy_switches_bounded_by_windows(orc):
     sc = BASE
     log, res = orc.scenario(sc)
     T, D, K, t0, t1 = sc["period"], sc["window_ticks"], sc["K"], sc["slow_t0"], sc["slow_t1"]
-    assert [(to, why) for _, _, to, why in log] == [(1, 1), (0, 2), (1, 0)]
+    assert [(to, why) for _, _, to, why, _ in log] == [(1, 1), (0, 2), (1, 0)]
     assert t0 + K * D <= log[0][0] <= t0 + (K + 1) * D + 4 * T
     assert t1 + K * D <= log[1][0] <= t1 + (K + 1) * D + 4 * T
     assert res["dropped"] == sc["n_workers"]
     assert (res["bsp_steps"], res["asp_pushes"]) == (2000, 48000)
     assert res["version"] == 2000 + 48000
+
+
+def test_elastic_policy_rules(orc):
+    # the detected straggler leaves the BSP barrier (K flagged windows into the transient), BSP continues
+    # with n - 1 workers until the BSP quota is met, then all n are restored and ASP runs the rest: one protocol
+    # switch in total, no dropped pushes.
+    sc = dict(BASE, policy=1)
+    log, res = orc.scenario(sc)
+    T, D, K, t0 = sc["period"], sc["window_ticks"], sc["K"], sc["slow_t0"]
+    assert [(to, why, m) for _, _, to, why, m in log] == [(0, 3, 7), (1, 0, 8)]
+    assert t0 + K * D <= log[0][0] <= t0 + (K + 1) * D + 4 * T
+    assert res["dropped"] == 0
+    quota = sc["total_samples"] * sc["quota_num"] // sc["quota_den"]
+    removal_version = log[0][1]
+    bsp_samples = removal_version * 8 * 128 + (res["bsp_steps"] - removal_version) * 7 * 128
+    assert bsp_samples >= quota and bsp_samples - 7 * 128 < quota          # the quota is met exactly once
+    assert res["asp_pushes"] * 128 + bsp_samples >= sc["total_samples"]
+    # A straggler that stays slow through the BSP phase holds every BSP superstep to 4000 ticks unless removed: then
+    # the elastic run finishes first. (A short transient can favour no policy, because the removed worker stays out
+    # until the quota is met, by design.)
+    persistent = dict(sc, slow_t1=10 ** 12)
+    assert orc.scenario(persistent)[1]["end_tick"] < orc.scenario(dict(persistent, policy=2))[1]["end_tick"]
+
+
+def test_elastic_bsp_equals_smaller_cluster(orc):
+    # BSP over m of n workers == BSP of an m-worker cluster (configuration policy re-derived for m)
+    rng = np.random.default_rng(31)
+    P, n = 257, 6
+    members = [0, 2, 3, 5]
+    w0 = rng.standard_normal(P).astype(np.float32)
+    gs = [[rng.standard_normal(P).astype(np.float32) for _ in range(n)] for _ in range(3)]
+    a = orc.Oracle(w0, 3, n, 0.05, 0.9)
+    assert a.set_members(members) == 0
+    b = orc.Oracle(w0, 3, len(members), 0.05, 0.9)
+    for r in range(3):
+        assert a.bsp_step([gs[r][j] for j in members], workers=members) == 0
+        assert b.bsp_step([gs[r][j] for j in members]) == 0
+    assert np.array_equal(a.params(), b.params()) and np.array_equal(a.velocity(), b.velocity())
+    assert a.bsp_step([gs[0][j] for j in range(n)]) == 3          # a removed worker at the barrier: SS_E_PROTOCOL
+    assert a.set_members([0, 0]) == 1 and a.set_members([]) == 1 and a.set_members([6]) == 1
 
 
 def test_quota_edge_cases(orc):
@@ -79,6 +124,16 @@ def test_quota_edge_cases(orc):
                                 dict(BASE, n_workers=4, slow_worker=1, total_samples=3000 * 128, quota_num=1,
                                      quota_den=3, slow_t0=5000, slow_t1=40000, K=2, window_ticks=6000, jitter=50)])
 def test_scenario_on_gpu_bit_exact(ss, orc, sc):
+    _scenario_on_gpu(ss, orc, sc)
+
+
+@pytest.mark.gpu
+def test_elastic_scenario_on_gpu_bit_exact(ss, orc):
+    _scenario_on_gpu(ss, orc, dict(BASE, policy=1, total_samples=4000 * 128, quota_num=1, quota_den=2,
+                                   slow_t0=10000, slow_t1=60000))
+
+
+def _scenario_on_gpu(ss, orc, sc):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
