@@ -232,6 +232,15 @@ ss_status ss_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t
 ss_status ss_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
                           float *grad, float *loss_dev, void *stream);
 
+/* Dynamic switching criterion for the toy model (SV §8(f) NEXT-3): computes the batch gradient at W,
+ * g_out = X^T (softmax(XW) - Y) / B (device fp32[d*C]), Delta = g_out - g_prev (g_prev: device fp32[d*C], the batch
+ * gradient k steps earlier on another batch, P:233-235 with reading C18), and writes stats (device fp32[2]) =
+ * {|Delta|, sigma} with sigma = sqrt(sum_b [Delta^T (grad_b - g)]^2) / (B |Delta|) over the batch's per-sample
+ * gradients grad_b (sigma = 0 when Delta = 0). The per-sample projections use the rank-one form
+ * grad_b = x_b (x) (p_b - y_b); sums accumulate in fp64 in a fixed order. B in [2, 1024], C <= 32. */
+ss_status ss_dynamic_criterion(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                               const float *g_prev, float *g_out, float *stats, void *stream);
+
 /* ============================================================================================================
  * Control plane (host only; no GPU needed)
  * ============================================================================================================ */
@@ -277,6 +286,11 @@ typedef struct {
 ss_status ss_route_plan(int32_t rank, int32_t world, int32_t n_workers, int32_t n_shards, int64_t n_params,
                         int32_t max_window, int32_t fused, const int32_t *kind, const int32_t *worker, int64_t n_ev,
                         ss_route_op *ops, int64_t cap, int64_t *n_ops, int32_t *n_windows);
+
+/* Persistence rule of the dynamic criterion ("we switch from BSP to ASP at the first time i when
+ * |Delta_i| < c sigma_i ... or once this criterion is satisfied for some number T steps in a row"): updates the
+ * consecutive-satisfied count *run (|Delta| = 0 counts as satisfied) and returns 1 when it reaches T. */
+int32_t ss_criterion_observe(int32_t *run, float norm_delta, float sigma, float c, int32_t T);
 
 /* Greedy online policy: given the detector's verdict, the protocol and the BSP quota, returns the switch
  * to issue now: -1 none, SS_ASP (a straggler appeared during BSP), SS_BSP (cluster clean, ASP, BSP quota unmet). */

@@ -341,3 +341,48 @@ def scenario(sc: dict, state: "Oracle | None" = None, P: int = 0, cap: int = 256
                              _ptr(res))
     keys = ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version", "windows", "n_switches")
     return [tuple(int(x) for x in r) for r in log[:min(nsw, cap)]], dict(zip(keys, (int(x) for x in res)))
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# dynamic switching criterion
+def _crit_sigs(L):
+    if not hasattr(L, "_crit"):
+        L.orc_criterion.argtypes = [_p, _i32, _i64, _p, _p, _p]
+        L.orc_softmax_per_sample.argtypes = [_p, _p, _i32, _i32, _i32, _p, _p]
+        L.orc_criterion_observe.restype = _i32
+        L.orc_criterion_observe.argtypes = [_p, _f64, _f64, _f64, _i32]
+        L._crit = True
+    return L
+
+
+def criterion(per_sample, g_prev):
+    """(|Delta|, sigma) from a B x P matrix of per-sample gradients and the lagged batch gradient."""
+    L = _crit_sigs(lib())
+    ps = np.ascontiguousarray(per_sample, dtype=np.float64)
+    gp = np.ascontiguousarray(g_prev, dtype=np.float64)
+    B, P = ps.shape
+    nd = np.zeros(1)
+    sg = np.zeros(1)
+    L.orc_criterion(_ptr(ps), B, P, _ptr(gp), _ptr(nd), _ptr(sg))
+    return float(nd[0]), float(sg[0])
+
+
+def softmax_per_sample(X, y, W):
+    L = _crit_sigs(lib())
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    B, d = X.shape
+    C = W.size // d
+    out = np.zeros((B, d * C))
+    L.orc_softmax_per_sample(_ptr(X), _ptr(y), B, d, C, _ptr(W), _ptr(out))
+    return out
+
+
+class CriterionRule:
+    def __init__(self, c: float = 2.0, T: int = 5):
+        self.c, self.T = c, T
+        self._run = np.zeros(1, dtype=np.int32)
+
+    def observe(self, norm_delta: float, sigma: float) -> bool:
+        return bool(_crit_sigs(lib()).orc_criterion_observe(_ptr(self._run), norm_delta, sigma, self.c, self.T))

@@ -429,3 +429,65 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
   orc_detector_free(det);
   return nlog;
 }
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Dynamic switching criterion (draft design P:226-243; reading C18: g is the per-sample MEAN, lag x_{i-k}).
+ * Written literally: per-sample gradients are materialised, then
+ *   g = (1/B) sum_b grad_b,  Delta = g - g_prev,
+ *   sigma = 1/(B |Delta|) * sqrt( sum_b [Delta^T (grad_b - g)]^2 )
+ * per_sample: B x P row-major. sigma = 0 when |Delta| = 0. */
+void orc_criterion(const double *per_sample, int32_t B, int64_t P, const double *g_prev, double *norm_delta,
+                   double *sigma) {
+  double *g = (double *)calloc((size_t)P, sizeof(double));
+  double *delta = (double *)malloc((size_t)P * sizeof(double));
+  for (int32_t b = 0; b < B; b++)
+    for (int64_t k = 0; k < P; k++) g[k] += per_sample[(int64_t)b * P + k];
+  for (int64_t k = 0; k < P; k++) g[k] /= (double)B;
+  double nd2 = 0.0;
+  for (int64_t k = 0; k < P; k++) {
+    delta[k] = g[k] - g_prev[k];
+    nd2 += delta[k] * delta[k];
+  }
+  double ss = 0.0;
+  for (int32_t b = 0; b < B; b++) {
+    double proj = 0.0;                                  /* Delta^T (grad_b - g) */
+    for (int64_t k = 0; k < P; k++) proj += delta[k] * (per_sample[(int64_t)b * P + k] - g[k]);
+    ss += proj * proj;
+  }
+  *norm_delta = sqrt(nd2);
+  *sigma = nd2 > 0.0 ? sqrt(ss) / ((double)B * sqrt(nd2)) : 0.0;
+  free(g);
+  free(delta);
+}
+
+/* Per-sample gradients of the softmax-regression loss -log p_{y_b}(x_b W): grad_b[i, c] = x_b[i] (p_b[c] - [c == y_b]).
+ * out: B x (d*C) row-major, fp64. */
+void orc_softmax_per_sample(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const double *W,
+                            double *out) {
+  double *z = (double *)malloc((size_t)C * sizeof(double));
+  for (int32_t b = 0; b < B; b++) {
+    const float *x = X + (int64_t)b * d;
+    for (int32_t c = 0; c < C; c++) {
+      double acc = 0.0;
+      for (int32_t i = 0; i < d; i++) acc += (double)x[i] * W[(int64_t)i * C + c];
+      z[c] = acc;
+    }
+    double m = z[0];
+    for (int32_t c = 1; c < C; c++) if (z[c] > m) m = z[c];
+    double den = 0.0;
+    for (int32_t c = 0; c < C; c++) den += exp(z[c] - m);
+    for (int32_t c = 0; c < C; c++) {
+      double r = exp(z[c] - m) / den - (c == y[b] ? 1.0 : 0.0);
+      for (int32_t i = 0; i < d; i++) out[(int64_t)b * d * C + (int64_t)i * C + c] = (double)x[i] * r;
+    }
+  }
+  free(z);
+}
+
+/* "we switch from BSP to ASP at the first time i when |Delta_i| < c sigma_i ... (or perhaps once this criterion is
+ * satisfied for some number T steps in a row)". |Delta| = 0 counts as satisfied. */
+int32_t orc_criterion_observe(int32_t *run, double norm_delta, double sigma, double c, int32_t T) {
+  int32_t satisfied = norm_delta == 0.0 || norm_delta < c * sigma;
+  *run = satisfied ? *run + 1 : 0;
+  return *run >= T;
+}

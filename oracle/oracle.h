@@ -114,6 +114,13 @@ int64_t orc_scenario_run(orc_f *st, int64_t P, int32_t n, int64_t B, int64_t W, 
                          int64_t slow_factor, int64_t slow_t0, int64_t slow_t1, int64_t D, int32_t K,
                          int32_t policy, int64_t *log5, int32_t cap, int64_t *res7);
 
+/* ---- dynamic switching criterion (reading C18), fp64, literal ---- */
+void orc_criterion(const double *per_sample, int32_t B, int64_t P, const double *g_prev, double *norm_delta,
+                   double *sigma);
+void orc_softmax_per_sample(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const double *W,
+                            double *out);
+int32_t orc_criterion_observe(int32_t *run, double norm_delta, double sigma, double c, int32_t T);
+
 #ifdef __cplusplus
 }
 #endif

@@ -256,6 +256,15 @@ ss_status ss_route_plan(int32_t rank, int32_t world, int32_t n_workers, int32_t 
   return SS_OK;
 }
 
+// Dynamic switching rule: satisfied when |Delta| < c*sigma (|Delta| = 0 counts as satisfied);
+// fires after T consecutive satisfied steps.
+int32_t ss_criterion_observe(int32_t *run, float norm_delta, float sigma, float c, int32_t T) {
+  if (!run || T < 1) return 0;
+  const bool ok = norm_delta == 0.0f || (double)norm_delta < (double)c * (double)sigma;
+  *run = ok ? *run + 1 : 0;
+  return *run >= T;
+}
+
 // Greedy policy: "simply switches to ASP ... when a straggler is detected; once the cluster is free of any
 // stragglers and the aggregate BSP training has not been satisfied, it will switch back to training with BSP".
 int32_t ss_greedy_decision(int32_t protocol, int32_t any_straggler, int32_t cluster_clean, int64_t bsp_done,

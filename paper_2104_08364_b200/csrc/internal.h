@@ -98,6 +98,9 @@ cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s);
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
                               cudaStream_t s);
+cudaError_t launch_dynamic_criterion(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C,
+                                     const float *W, const float *g_prev, float *g_out, float *stats, float *scratch,
+                                     double *part, cudaStream_t s);
 cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
                                 float *grad, float *loss, float *scratch, cudaStream_t s);
 

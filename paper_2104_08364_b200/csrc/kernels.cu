@@ -678,6 +678,72 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float *X, i
   }
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// Dynamic switching criterion for the toy model. With per-sample gradients
+// grad_b = x_b (x) (p_b - y_b) (rank one) and the batch mean g, Delta = g - g_prev:
+//   u_b = Delta^T (grad_b - g) = x_b^T Delta (p_b - y_b) - Delta^T g,  sigma = sqrt(sum_b u_b^2) / (B |Delta|).
+// r = (p - y)/B from softmax_fwd, so x_b^T Delta (p_b - y_b) = B * sum_i x_b[i] sum_c Delta[i,c] r[b,c]. One CTA per
+// sample (plus one for |Delta|^2 and Delta^T g), fp64 accumulation in a fixed order; a final 1-CTA kernel.
+__global__ void __launch_bounds__(kThreads) criterion_partial_kernel(const float *X, int32_t B, int32_t d, int32_t C,
+                                                                     const float *r, const float *g,
+                                                                     const float *g_prev, double *part) {
+  const int b = blockIdx.x;  // b < B: sample b; b == B: global terms
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    if (b < B) {
+      double t = 0.0;
+      for (int c = 0; c < C; ++c) {
+        const int64_t k = (int64_t)i * C + c;
+        t += (double)(g[k] - g_prev[k]) * (double)r[(int64_t)b * C + c];
+      }
+      acc0 += (double)X[(int64_t)b * d + i] * t;
+    } else {
+      for (int c = 0; c < C; ++c) {
+        const int64_t k = (int64_t)i * C + c;
+        const double dl = (double)g[k] - (double)g_prev[k];
+        acc0 += dl * dl;
+        acc1 += dl * (double)g[k];
+      }
+    }
+  }
+  __shared__ double red0[kThreads / 32], red1[kThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    acc0 += __shfl_down_sync(0xffffffffu, acc0, o);
+    acc1 += __shfl_down_sync(0xffffffffu, acc1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red0[threadIdx.x >> 5] = acc0;
+    red1[threadIdx.x >> 5] = acc1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      s0 += red0[w];
+      s1 += red1[w];
+    }
+    if (b < B) {
+      part[b] = s0 * (double)B;        // x_b^T Delta (p_b - y_b)
+    } else {
+      part[B] = s0;                    // |Delta|^2
+      part[B + 1] = s1;                // Delta^T g
+    }
+  }
+}
+
+__global__ void criterion_final_kernel(int32_t B, const double *part, float *stats) {
+  if (threadIdx.x != 0) return;
+  const double nd2 = part[B], dg = part[B + 1];
+  double su = 0.0;
+  for (int b = 0; b < B; ++b) {
+    const double u = part[b] - dg;
+    su += u * u;
+  }
+  const double nd = sqrt(nd2);
+  stats[0] = (float)nd;
+  stats[1] = nd > 0.0 ? (float)(sqrt(su) / ((double)B * nd)) : 0.0f;
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (g_num_sms == 0) {
@@ -788,6 +854,17 @@ cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, i
   int64_t want = (items + kThreads - 1) / kThreads;
   int64_t cap = (int64_t)num_sms() * 8;
   synth_grad_kernel<<<(int)(want < cap ? want : cap), kThreads, 0, s>>>(seed, jk, i0, count, dst, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dynamic_criterion(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C,
+                                     const float *W, const float *g_prev, float *g_out, float *stats, float *scratch,
+                                     double *part, cudaStream_t s) {
+  float *loss = scratch + (int64_t)B * (C + 1);
+  cudaError_t e = launch_softmax_grad(X, y, B, d, C, W, g_out, loss, scratch, s);  // r in scratch[0 .. B*C)
+  if (e != cudaSuccess) return e;
+  criterion_partial_kernel<<<B + 1, kThreads, 0, s>>>(X, B, d, C, scratch, g_out, g_prev, part);
+  criterion_final_kernel<<<1, 32, 0, s>>>(B, part, stats);
   return cudaGetLastError();
 }
 

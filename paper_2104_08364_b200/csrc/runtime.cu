@@ -1125,6 +1125,21 @@ ss_status ss_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t
   return ss::launch_synth_grad(seed, j, k, i0, count, dst, (cudaStream_t)stream) == cudaSuccess ? SS_OK : SS_E_CUDA;
 }
 
+ss_status ss_dynamic_criterion(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
+                               const float *g_prev, float *g_out, float *stats, void *stream) {
+  if (!X || !y || !W || !g_prev || !g_out || !stats || B < 2 || B > 1024 || d < 1 || C < 1 || C > 32)
+    return SS_E_INVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  float *scratch = nullptr;
+  double *part = nullptr;
+  if (cudaMallocAsync(&scratch, ((size_t)B * (C + 1) + 1) * sizeof(float), s) != cudaSuccess) return SS_E_OOM;
+  if (cudaMallocAsync(&part, (size_t)(B + 2) * sizeof(double), s) != cudaSuccess) return SS_E_OOM;
+  cudaError_t e = ss::launch_dynamic_criterion(X, y, B, d, C, W, g_prev, g_out, stats, scratch, part, s);
+  cudaFreeAsync(scratch, s);
+  cudaFreeAsync(part, s);
+  return e == cudaSuccess ? SS_OK : SS_E_CUDA;
+}
+
 ss_status ss_softmax_grad(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C, const float *W,
                           float *grad, float *loss, void *stream) {
   if (!X || !y || !W || !grad || !loss || B < 1 || B > 1024 || d < 1 || C < 1 || C > 32) return SS_E_INVAL;

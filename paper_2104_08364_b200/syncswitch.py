@@ -31,7 +31,8 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
            "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer",
-           "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked"]
+           "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked",
+           "ss_dynamic_criterion", "ss_criterion_observe"]
 
 
 class SSError(RuntimeError):
@@ -107,6 +108,7 @@ def _load():
         "ss_kernel_stats": [p, i32, p, p, p],
         "ss_synth_grad": [u64, i32, i64, i64, i64, p, p],
         "ss_softmax_grad": [p, p, i32, i32, i32, p, p, p, p],
+        "ss_dynamic_criterion": [p, p, i32, i32, i32, p, p, p, p, p],
         "ss_table1": [i64, i64, i64, i64, i64, p, i32, p, p, p],
         "ss_schedule": [i32, p, i64, u64, i32, i64, i64, i64, i64, p, p, p, p],
         "ss_detector_new": [p, i32, i32],
@@ -124,6 +126,8 @@ def _load():
     L.ss_detector_free.restype = None
     L.ss_last_error.argtypes = [p]
     L.ss_last_error.restype = ctypes.c_char_p
+    L.ss_criterion_observe.argtypes = [p, f32, f32, f32, i32]
+    L.ss_criterion_observe.restype = i32
     L.ss_greedy_decision.argtypes = [i32, i32, i32, i64, i64]
     L.ss_greedy_decision.restype = i32
     return L
@@ -297,6 +301,21 @@ def ss_synth_grad(seed: int, j: int, k: int, i0: int, count: int, dst, stream: i
 
 def ss_softmax_grad(X, y, B: int, d: int, C: int, W, grad, loss, stream: int = 0) -> int:
     return lib.ss_softmax_grad(ptr(X), ptr(y), B, d, C, ptr(W), ptr(grad), ptr(loss), stream or None)
+
+
+def ss_dynamic_criterion(X, y, B: int, d: int, C: int, W, g_prev, g_out, stats, stream: int = 0) -> int:
+    return lib.ss_dynamic_criterion(ptr(X), ptr(y), B, d, C, ptr(W), ptr(g_prev), ptr(g_out), ptr(stats),
+                                    stream or None)
+
+
+class CriterionRule:
+    """ss_criterion_observe: fires after T consecutive steps with |Delta| < c sigma."""
+
+    def __init__(self, c: float = 2.0, T: int = 5):
+        self.c, self.T, self._run = c, T, ctypes.c_int32(0)
+
+    def observe(self, norm_delta: float, sigma: float) -> bool:
+        return bool(lib.ss_criterion_observe(ctypes.byref(self._run), norm_delta, sigma, self.c, self.T))
 
 
 def ss_table1(W: int, B: int, N: int, s_num: int, s_den: int, Wb):
