@@ -16,11 +16,12 @@ RESNET32_P = 464_154      # ResNet-32 / CIFAR-10 shaped (computed in SURVEY §8;
 RESNET50_P = 25_557_032   # ResNet-50 shaped (torchvision, BASELINE.json "25.6M")
 
 
-def toy_dataset(seed: int = 1, n_points: int = 1000, d: int = 1024, C: int = 8):
+def toy_dataset(seed: int = 1, n_points: int = 1000, d: int = 1024, C: int = 8, mean_scale: float = 0.5):
     """Config 1 data: a Gaussian mixture of C classes in d-1 dims plus a constant-1 bias feature (P = d*C).
-    Class means ~ N(0, I) scaled by 0.5, unit-variance noise; labels uniform. Returns X float32 [N, d], y int32."""
+    Class means ~ N(0, I) scaled by `mean_scale` (0.5: separable; 0.05: overlapping classes, the gradient noise never
+    vanishes), unit-variance noise; labels uniform. Returns X float32 [N, d], y int32."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    means = rng.standard_normal((C, d - 1)) * 0.5
+    means = rng.standard_normal((C, d - 1)) * mean_scale
     y = rng.integers(0, C, n_points).astype(np.int32)
     X = means[y] + rng.standard_normal((n_points, d - 1))
     X = np.concatenate([X, np.ones((n_points, 1))], axis=1).astype(np.float32)

@@ -653,10 +653,16 @@ __global__ void __launch_bounds__(kThreads) softmax_fwd_kernel(const float *X, c
     for (int c = 0; c < C; ++c) den += expf(z[c] - m);
     const int yb = y[b];
     loss_b[b] = -((z[yb] - m) - logf(den));
+    // r = (p - onehot(y)) / B. For the true class p_y - 1 = -sum_{c != y} p_c: summing the other classes avoids the
+    // cancellation of p_y - 1 in fp32 when the model is confident (p_y -> 1).
+    float rest = 0.0f;
     for (int c = 0; c < C; ++c) {
+      if (c == yb) continue;
       const float p = expf(z[c] - m) / den;
-      r[(int64_t)b * C + c] = (p - (c == yb ? 1.0f : 0.0f)) / (float)B;
+      rest += p;
+      r[(int64_t)b * C + c] = p / (float)B;
     }
+    r[(int64_t)b * C + yb] = -rest / (float)B;
   }
 }
 
