@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <unordered_map>
 
 #include "internal.h"
 
@@ -578,6 +579,140 @@ __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------------------------------------------
+// pipe_bsp (fused BSP, pipelined): see PipeBspArgs. The grid is split in two roles. Phase-A CTAs (the first half)
+// claim items (chunk c of rank q's region, c-major so every link carries traffic from the start) from counter 0 and
+// never wait; phase-B CTAs claim chunks of this rank's region from counter 1, in order, and wait only for that
+// chunk's flags — so early chunks are reduced, updated and broadcast while later chunks are still in flight, and no
+// wait can deadlock (every rank's phase A runs to completion). Phase B sums its terms in the fixed ascending order.
+__device__ __forceinline__ void chunk_copy(float *dst, const float *src, int64_t len) {
+  const int64_t n4 = len >> 2;
+  for (int64_t q = threadIdx.x; q < n4; q += 2 * kThreads) {
+    const bool two = q + kThreads < n4;
+    const float4 x0 = ld4(src + 4 * q);
+    float4 x1;
+    if (two) x1 = ld4(src + 4 * (q + kThreads));
+    *reinterpret_cast<float4 *>(dst + 4 * q) = x0;
+    if (two) *reinterpret_cast<float4 *>(dst + 4 * (q + kThreads)) = x1;
+  }
+  for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += kThreads) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constant__ PipeBspArgs a) {
+  __shared__ uint32_t s_item;
+  const int me = a.sync.rank, G = a.sync.world;
+  const uint32_t nA = (uint32_t)(G * a.max_chunks);
+  const uint32_t nB = (uint32_t)a.n_chunks[me];
+  const bool roleA = blockIdx.x < (gridDim.x + 1) / 2;
+  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
+  bool bad = false;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(a.work + (roleA ? 0 : 1), 1u);
+    __syncthreads();
+    const uint32_t it = roleA ? s_item : nA + s_item;
+    __syncthreads();
+    if (roleA ? it >= nA : it >= nA + nB) break;
+    if (it < nA) {
+      // ---------------- phase A: chunk c of rank q's region ----------------
+      const int c = (int)(it / G), q = (int)(it % G);
+      if (c >= a.n_chunks[q] || (q == me && !a.presum)) continue;
+      const int64_t off = (int64_t)c * a.chunk_len[q];
+      const int64_t len = min(a.chunk_len[q], a.cnt[q] - off);
+      const int64_t gsrc = a.real_lo[q] + off;       // position in the full vector
+      if (a.presum) {
+        float *dst = a.inbox[q] + (int64_t)me * a.reg_len + off;
+        const int64_t n4 = len >> 2;
+        for (int64_t p = threadIdx.x; p < n4; p += kThreads) {
+          float4 acc = a.n_src > 0 ? ld4(a.src[0] + gsrc + 4 * p) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 1; k < a.n_src; ++k) acc = add4(acc, ld4(a.src[k] + gsrc + 4 * p));
+          *reinterpret_cast<float4 *>(dst + 4 * p) = acc;
+        }
+        for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += kThreads) {
+          float acc = a.n_src > 0 ? a.src[0][gsrc + i] : 0.0f;
+          for (int k = 1; k < a.n_src; ++k) acc = __fadd_rn(acc, a.src[k][gsrc + i]);
+          dst[i] = acc;
+        }
+      } else {
+        for (int k = 0; k < a.n_src; ++k)
+          chunk_copy(a.inbox[q] + (int64_t)a.slot[k] * a.reg_len + off, a.src[k] + gsrc, len);
+      }
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_sys(a.flags[q] + c * kMaxPeers + me, a.epoch);
+    } else {
+      // ---------------- phase B: chunk c of this rank's region ----------------
+      const int c = (int)(it - nA);
+      if (threadIdx.x == 0) {
+        const unsigned long long t0 = globaltimer();
+        for (int q = 0; q < G; ++q) {
+          if (q == me && !a.presum) continue;
+          const uint32_t *f = a.flags[me] + c * kMaxPeers + q;
+          while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+            if (globaltimer() - t0 > kTimeoutNs) {
+              atomicExch(a.sync.err, 1);
+              break;
+            }
+            __nanosleep(64);
+          }
+        }
+      }
+      __syncthreads();
+      const int64_t off = (int64_t)c * a.chunk_len[me];
+      const int64_t len = min(a.chunk_len[me], a.cnt[me] - off);
+      const int64_t n4 = len >> 2;
+      for (int64_t p = threadIdx.x; p < n4; p += kThreads) {
+        const int64_t e = off + 4 * p;
+        float4 acc = ld4(a.g[0] + e);
+        for (int j0 = 1; j0 < a.n_in; j0 += kG1) {
+          float4 t[kG1];
+#pragma unroll
+          for (int jj = 0; jj < kG1; ++jj)
+            if (j0 + jj < a.n_in) t[jj] = ld4(a.g[j0 + jj] + e);
+#pragma unroll
+          for (int jj = 0; jj < kG1; ++jj)
+            if (j0 + jj < a.n_in) acc = add4(acc, t[jj]);     // ascending order
+        }
+        float4 wv = ld4(a.w + e), vv = ld4(a.v + e);
+        up(acc.x, wv.x, vv.x);
+        up(acc.y, wv.y, vv.y);
+        up(acc.z, wv.z, vv.z);
+        up(acc.w, wv.w, vv.w);
+        bad |= nonfinite(wv.x) | nonfinite(wv.y) | nonfinite(wv.z) | nonfinite(wv.w) | nonfinite(vv.x) |
+               nonfinite(vv.y) | nonfinite(vv.z) | nonfinite(vv.w);
+        st4(a.w + e, wv);
+        st4(a.v + e, vv);
+        for (int b = 0; b < a.n_bcast; ++b) *reinterpret_cast<float4 *>(a.bcast[b] + e) = wv;
+      }
+      for (int64_t i = off + 4 * n4 + threadIdx.x; i < off + len; i += kThreads) {
+        float acc = a.g[0][i];
+        for (int j = 1; j < a.n_in; ++j) acc = __fadd_rn(acc, a.g[j][i]);
+        float w = a.w[i], v = a.v[i];
+        up(acc, w, v);
+        bad |= nonfinite(w) | nonfinite(v);
+        a.w[i] = w;
+        a.v[i] = v;
+        for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+  // end barrier; the last CTA also rewinds the item counter for the next step
+  __threadfence_system();
+  __syncthreads();
+  __shared__ uint32_t last;
+  if (threadIdx.x == 0) last = atomicAdd(a.sync.ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) {
+    *a.sync.ctr = 0;
+    a.work[0] = 0;
+    a.work[1] = 0;
+    __threadfence_system();
+    for (int q = 0; q < G; ++q) st_release_sys(a.sync.sig_peer[q] + me, a.sync.signal_epoch);
+  }
+  peer_wait(a.sync, a.sync.signal_epoch);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
 // K3 synth_grad: g = ((h >> 40) * 2^-24 - 0.5) * 2^-6 with h = splitmix64(seed ^ ((j<<56) ^ (k<<30) ^ i)).
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -764,13 +899,17 @@ int num_sms() {
 // Grid: enough CTAs for the work, capped at (resident CTAs per SM) x (SM count) — one full wave of a persistent
 // grid-stride kernel (B200: 148 SMs).
 // Resident CTAs per SM, queried once per kernel (a host API call per launch would dominate small launches).
+// Keyed by the kernel's address: kernels of the same signature share a function-pointer type.
 template <typename K>
 int resident_ctas(K kernel) {
-  static int r = 0;
-  if (r == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
-    if (r <= 0) r = 1;
-  }
+  static std::unordered_map<const void *, int> cache;
+  const void *key = reinterpret_cast<const void *>(kernel);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int r = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kernel, kThreads, 0);
+  if (r <= 0) r = 1;
+  cache[key] = r;
   return r;
 }
 
@@ -835,6 +974,13 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     auto k = asp_replay_kernel<false>;
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s) {
+  auto k = pipe_bsp_kernel;
+  const int grid = resident_ctas(k) * num_sms();   // persistent: every CTA resident (items are claimed dynamically)
+  k<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -311,8 +312,8 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
   if (!c->pbuf) SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
   if (!c->sigblk) {
-    SS_CUDA(c, cudaMalloc(&c->sigblk, 256 * sizeof(uint32_t)));
-    SS_CUDA(c, cudaMemset(c->sigblk, 0, 256 * sizeof(uint32_t)));
+    SS_CUDA(c, cudaMalloc(&c->sigblk, ss::kSigWords * sizeof(uint32_t)));
+    SS_CUDA(c, cudaMemset(c->sigblk, 0, ss::kSigWords * sizeof(uint32_t)));
   }
   c->inbox_slots = slots;
   cudaIpcMemHandle_t mine[4];
@@ -769,6 +770,15 @@ ss_status ss_current_lr(ss_ctx *c, int32_t proto, float *lr_out) {
   return SS_OK;
 }
 
+// The pipelined fused BSP kernel (pipe_bsp) is kept for experiments; the two-kernel form measured faster so far.
+bool bsp_pipe_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SS_BSP_PIPE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *workers, const int64_t *versions,
                       int32_t n_local) {
   SS_TRY(check_live(c));
@@ -823,6 +833,63 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     Timed t;
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
+    timed_end(c, &t);
+  } else if (c->fused_mode != 0 && bsp_pipe_enabled()) {
+    // Fused peer-memory BSP, pipelined (experimental, SS_BSP_PIPE=1; kernels.cu pipe_bsp): one persistent kernel per rank.
+    // Phase-A items store chunk slices of this rank's hosted gradients (mode 1) or of their ascending pre-sum (mode 2)
+    // into the owners' inboxes and raise per-chunk flags; phase-B items reduce, update and broadcast each chunk of the
+    // owned region as soon as its flags are up. One end barrier closes the step.
+    const bool presum = c->fused_mode == 2;
+    SS_TRY(ensure_fused(c, presum ? c->world : c->n));
+    const uint32_t epA = ++c->epoch, epB = ++c->epoch;
+    const int32_t me = c->rank;
+    const int64_t lo = c->real_lo[me];
+    ss::PipeBspArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    pa.n_src = k;
+    for (int32_t i = 0; i < k; ++i) {
+      if (!aligned16(a.g[i])) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
+      pa.src[i] = a.g[i];
+      pa.slot[i] = ids[i];
+    }
+    pa.presum = presum ? 1 : 0;
+    pa.reg_len = c->reg_len;
+    for (int32_t q = 0; q < c->world; ++q) {
+      pa.inbox[q] = c->peer_inbox[q];
+      pa.flags[q] = c->peer_sig[q] + ss::kSigChunkBase;
+      pa.real_lo[q] = c->real_lo[q];
+      pa.cnt[q] = c->real_hi[q] - c->real_lo[q];
+      int64_t nch = pa.cnt[q] > 0 ? std::min<int64_t>(ss::kMaxChunks, (pa.cnt[q] + 65535) / 65536) : 0;
+      pa.chunk_len[q] = nch > 0 ? ((pa.cnt[q] + nch - 1) / nch + 31) / 32 * 32 : 32;
+      pa.n_chunks[q] = nch > 0 ? (int32_t)((pa.cnt[q] + pa.chunk_len[q] - 1) / pa.chunk_len[q]) : 0;
+      pa.max_chunks = std::max(pa.max_chunks, pa.n_chunks[q]);
+    }
+    int32_t ni = 0, h = 0;
+    if (presum) {
+      for (int32_t q = 0; q < c->world; ++q) pa.g[ni++] = c->inbox + (int64_t)q * c->reg_len;
+    } else {
+      for (int32_t j = 0; j < c->n; ++j) {   // the members' slices, ascending worker order
+        if (!c->member[j]) continue;
+        pa.g[ni++] = host_of(c, j) == me ? a.g[h++] + lo : c->inbox + (int64_t)j * c->reg_len;
+      }
+    }
+    pa.n_in = ni;
+    pa.w = c->w + lo;
+    pa.v = c->v;
+    for (int32_t q = 0; q < c->world; ++q)
+      if (q != me) pa.bcast[pa.n_bcast++] = c->peer_w[q] + lo;
+    pa.flag = c->flag;
+    pa.divisor = a.divisor;
+    pa.mu = a.mu;
+    pa.neg_eta = a.neg_eta;
+    pa.lam = a.lam;
+    pa.work = c->sigblk + 96;
+    pa.epoch = epA;
+    pa.sync = peer_sync(c, 0, epB, true);
+    Timed t;
+    const double cnt_me = (double)(c->real_hi[me] - lo);
+    timed_begin(c, &t, 0, 4.0 * cnt_me * (ni + 4));
+    SS_CUDA(c, ss::launch_pipe_bsp(pa, c->stream));
     timed_end(c, &t);
   } else if (c->fused_mode != 0) {
     // Fused peer-memory BSP. Phase A: scatter hosted gradients (exact mode) or this rank's
