@@ -211,11 +211,13 @@ ss_status ss_set_window(ss_ctx *ctx, int32_t max_events);
 ss_status ss_get_stream(ss_ctx *ctx, void **stream_out);
 /* Order the context's work after `stream` (cudaStream_t) — used when gradients are produced on another stream. */
 ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
-/* Kernel timing: when on, every bsp_update / asp_replay launch is bracketed by CUDA events on the context's stream;
- * ss_kernel_stats returns per-kernel launch count, total device milliseconds and algorithmic HBM bytes
- * (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum, 3 = scatter). Reading synchronizes. */
+/* Kernel timing: when on, every launch of the path's kernels is bracketed by CUDA events on the context's stream;
+ * ss_kernel_stats returns per-kernel launch count, total device milliseconds, algorithmic HBM bytes and algorithmic
+ * bytes sent over NVLink by the fused multi-GPU path (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum,
+ * 3 = scatter / scatter_sum). Any output may be NULL. Reading synchronizes. */
 ss_status ss_profile(ss_ctx *ctx, int32_t on);
-ss_status ss_kernel_stats(ss_ctx *ctx, int32_t kernel_id, int64_t *launches, double *total_ms, double *bytes);
+ss_status ss_kernel_stats(ss_ctx *ctx, int32_t kernel_id, int64_t *launches, double *total_ms, double *bytes,
+                          double *nvlink_bytes);
 
 /* ============================================================================================================
  * Seeded synthetic inputs and the toy model (SV §8d; kernels synth_grad and softmax_grad)

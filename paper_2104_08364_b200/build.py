@@ -13,9 +13,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsyncswitch.so")
-SOURCES = ["runtime.cu", "kernels.cu", "control.cpp", "scenario.cpp"]
+SOURCES = ["runtime.cu", "kernels.cu", "control.cpp", "scenario.cpp", "nvls.cpp"]
 HEADERS_EXTRA = ["plan.h"]
-HEADERS = ["internal.h", "plan.h"]
+HEADERS = ["internal.h", "plan.h", "nvls.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -39,6 +39,7 @@ struct BspArgs {
   float lam;
   float *bcast[kMaxPeers];  // fused path: remote replicas (at this slice's offset) that receive the updated w
   int32_t n_bcast;
+  float *mc_w;              // NVLS: multicast view of this slice; one multimem.st updates every replica
   PeerSync sync;
 };
 

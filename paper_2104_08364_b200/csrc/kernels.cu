@@ -91,6 +91,16 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 
 __device__ __forceinline__ bool nonfinite(float x) { return !isfinite(x); }
 
+// NVLS: one store through the multicast view writes the value into every GPU's copy (switch replication).
+__device__ __forceinline__ void mc_st4(float *p, float4 x) {
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x.x), "f"(x.y), "f"(x.z),
+               "f"(x.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st1(float *p, float x) {
+  asm volatile("multimem.st.weak.global.f32 [%0], %1;" ::"l"(p), "f"(x) : "memory");
+}
+
 // g = a / divisor (+ lam*w); v = mu*v + g; w = w - eta*v.  When the divisor is a power of two, a*recip is the same
 // correctly rounded quotient, so `use_recip` changes no bit.
 struct Upd {
@@ -159,10 +169,14 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
         bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
                nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
         const int64_t q = q0 + u * stride;
-        st4(a.w + 4 * q, wv[u]);
+        if (a.mc_w) {
+          mc_st4(a.mc_w + 4 * q, wv[u]);        // NVLS: every replica, this GPU's included
+        } else {
+          st4(a.w + 4 * q, wv[u]);
+          for (int b = 0; b < a.n_bcast; ++b)   // fused path: the updated slice goes straight to every replica
+            *reinterpret_cast<float4 *>(a.bcast[b] + 4 * q) = wv[u];
+        }
         st4(a.v + 4 * q, vv[u]);
-        for (int b = 0; b < a.n_bcast; ++b)   // fused path: the updated slice goes straight to every replica
-          *reinterpret_cast<float4 *>(a.bcast[b] + 4 * q) = wv[u];
       }
     }
     // scalar tail (count % 4 elements)
@@ -173,9 +187,13 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       float w = a.w[i], v = a.v[i];
       up(acc, w, v);
       bad |= nonfinite(w) | nonfinite(v);
-      a.w[i] = w;
+      if (a.mc_w) {
+        mc_st1(a.mc_w + i, w);
+      } else {
+        a.w[i] = w;
+        for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
+      }
       a.v[i] = v;
-      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
     }
   } else {
     for (int64_t i = tid; i < a.count; i += stride) {
@@ -184,12 +202,17 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       float w = a.w[i], v = a.v[i];
       up(acc, w, v);
       bad |= nonfinite(w) | nonfinite(v);
-      a.w[i] = w;
+      if (a.mc_w) {
+        mc_st1(a.mc_w + i, w);
+      } else {
+        a.w[i] = w;
+        for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
+      }
       a.v[i] = v;
-      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
+  if (a.mc_w) asm volatile("fence.proxy.alias;" ::: "memory");  // multicast stores before unicast accesses
   peer_done(a.sync);
 }
 

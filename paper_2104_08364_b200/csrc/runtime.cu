@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "nvls.h"
 #include "plan.h"
 #include "syncswitch.h"
 
@@ -39,13 +40,14 @@ struct Ev {
 
 struct KStat {
   int64_t launches = 0;
-  double ms = 0.0, bytes = 0.0;
+  double ms = 0.0, bytes = 0.0, nvbytes = 0.0;
 };
 
 struct Timed {
   cudaEvent_t a, b;
   int kernel;
-  double bytes;
+  double bytes;    // algorithmic HBM bytes of the launch
+  double nvbytes;  // algorithmic bytes the launch sends over NVLink (fused multi-GPU path)
 };
 
 }  // namespace
@@ -106,6 +108,10 @@ struct ss_ctx {
   float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
   uint32_t *peer_sig[ss::kMaxPeers] = {};
   std::vector<void *> opened;          // peer mappings to close
+  ss::NvlsReplica nvls;                // NVSwitch multicast replica (w lives here when ready)
+  bool nvls_tried = false;
+  bool w_vmm = false;                  // w points into the NVLS replica (not cudaMalloc memory)
+  char job_tag[48] = {0};              // names the NVLS fd socket: hash of the NCCL unique id + setup count
   uint32_t epoch = 0;
   int32_t first_hosted = 0, n_hosted = 0;
   // instrumentation
@@ -239,10 +245,11 @@ cudaEvent_t pooled_event(ss_ctx *c) {
   return e;
 }
 
-void timed_begin(ss_ctx *c, Timed *t, int kernel, double bytes) {
+void timed_begin(ss_ctx *c, Timed *t, int kernel, double bytes, double nvbytes = 0.0) {
   if (!c->prof) return;
   t->kernel = kernel;
   t->bytes = bytes;
+  t->nvbytes = nvbytes;
   t->a = pooled_event(c);
   t->b = pooled_event(c);
   cudaEventRecord(t->a, c->stream);
@@ -263,6 +270,7 @@ ss_status drain_timed(ss_ctx *c) {
     c->kstat[t.kernel].launches += 1;
     c->kstat[t.kernel].ms += ms;
     c->kstat[t.kernel].bytes += t.bytes;
+    c->kstat[t.kernel].nvbytes += t.nvbytes;
     c->event_pool.push_back(t.a);
     c->event_pool.push_back(t.b);
   }
@@ -303,6 +311,50 @@ void close_ipc(ss_ctx *c, bool all) {
   }
 }
 
+// NVLS replica (collective, once): every rank checks support, all agree (NCCL min), then the multicast object is
+// created, shared and bound (nvls.cpp) and w moves into it. Any failure on any rank leaves every rank on the P2P
+// broadcast.
+ss_status agree_all(ss_ctx *c, int32_t *flag) {
+  int32_t *d = nullptr;
+  SS_CUDA(c, cudaMalloc(&d, sizeof(int32_t)));
+  SS_CUDA(c, cudaMemcpy(d, flag, sizeof(int32_t), cudaMemcpyHostToDevice));
+  SS_NCCL(c, ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  SS_CUDA(c, cudaMemcpyAsync(flag, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  return SS_OK;
+}
+
+ss_status ensure_nvls(ss_ctx *c) {
+  if (c->nvls_tried) return SS_OK;
+  c->nvls_tried = true;
+  // Default: on for world >= 8 only. Measured on this pool (tools/mc_bench.cu, profiles/r01_nvls_microbench.txt):
+  // at 4 GPUs a multicast store moves 181 GB/s of source data per GPU against 225 GB/s for P2P stores to all three
+  // peers; P2P is capped near 770/(G-1) GB/s of source, so multicast only wins from 8 GPUs on. SS_NVLS=0/1 overrides.
+  const char *env = getenv("SS_NVLS");
+  const bool want = env ? env[0] == '1' : c->world >= 8;
+  int32_t ok = want && ss::nvls_supported(c->device) ? 1 : 0;
+  SS_TRY(agree_all(c, &ok));
+  if (!ok) return SS_OK;
+  const char *why = ss::nvls_setup(&c->nvls, c->rank, c->world, c->device, (size_t)c->P_pad * sizeof(float),
+                                   c->job_tag);
+  ok = why == nullptr;
+  SS_TRY(agree_all(c, &ok));
+  if (!ok) {
+    if (why) fprintf(stderr, "syncswitch: NVLS multicast unavailable on rank %d (%s); using P2P stores\n", c->rank,
+                     why);
+    ss::nvls_release(&c->nvls);
+    return SS_OK;
+  }
+  SS_CUDA(c, cudaMemcpyAsync(c->nvls.uc, c->w, (size_t)c->P_pad * sizeof(float), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(c->w);
+  c->w = (float *)c->nvls.uc;
+  c->w_vmm = true;
+  return SS_OK;
+}
+
 ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   if (c->ipc_ready && c->inbox_slots >= slots) return SS_OK;
   if (c->world > ss::kMaxPeers) return fail(c, SS_E_INVAL, "fused path supports at most %d ranks", ss::kMaxPeers);
@@ -316,8 +368,10 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
     SS_CUDA(c, cudaMemset(c->sigblk, 0, ss::kSigWords * sizeof(uint32_t)));
   }
   c->inbox_slots = slots;
+  SS_TRY(ensure_nvls(c));
   cudaIpcMemHandle_t mine[4];
-  SS_CUDA(c, cudaIpcGetMemHandle(&mine[0], c->w));
+  std::memset(mine, 0, sizeof mine);
+  if (!c->w_vmm) SS_CUDA(c, cudaIpcGetMemHandle(&mine[0], c->w));  // an NVLS replica is reached by multicast
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[1], c->inbox));
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[2], c->pbuf));
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[3], c->sigblk));
@@ -338,8 +392,8 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
       c->peer_sig[q] = c->sigblk;
       continue;
     }
-    void *p[4];
-    for (int k = 0; k < 4; ++k) {
+    void *p[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int k = c->w_vmm ? 1 : 0; k < 4; ++k) {
       SS_CUDA(c, cudaIpcOpenMemHandle(&p[k], all[4 * q + k], cudaIpcMemLazyEnablePeerAccess));
       c->opened.push_back(p[k]);
     }
@@ -385,7 +439,10 @@ ss_status launch_scatter(ss_ctx *c, const std::vector<std::pair<const float *, i
   a.P = c->P;
   a.sync = peer_sync(c, 0, epoch, false);
   Timed t;
-  timed_begin(c, &t, 3, 8.0 * (double)c->P * (double)src.size() * (c->world - 1) / c->world);
+  double remote = 0.0;  // elements of the other ranks' regions
+  for (int32_t q = 0; q < c->world; ++q)
+    if (q != c->rank) remote += (double)(c->real_hi[q] - c->real_lo[q]);
+  timed_begin(c, &t, 3, 4.0 * remote * (double)src.size(), 4.0 * remote * (double)src.size());
   SS_CUDA(c, ss::launch_scatter(a, c->stream));
   timed_end(c, &t);
   return SS_OK;
@@ -417,9 +474,10 @@ ss_status flush_fused(ss_ctx *c) {
   ss::AspArgs a;
   std::memset(&a, 0, sizeof a);
   bool vec = true;
-  int32_t ne = 0, n_push = 0, n_pull = 0;
+  int32_t ne = 0, n_push = 0, n_pull = 0, n_remote_pull = 0;
   for (size_t k = 0; k < c->win.size(); ++k) {
     const Ev &e = c->win[k];
+    if (e.kind == 1 && e.data && host_of(c, e.worker) != me) ++n_remote_pull;
     ss::AspEvent &x = a.ev[ne];
     x.kind = e.kind;
     if (e.kind == 0) {
@@ -444,7 +502,7 @@ ss_status flush_fused(ss_ctx *c) {
   a.lam = c->lam;
   a.sync = peer_sync(c, epA, epB, true);
   Timed t;
-  timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
+  timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
   SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
   timed_end(c, &t);
   for (const Ev &e : c->win) {
@@ -677,6 +735,9 @@ ss_status ss_init_dist(ss_ctx *c, int32_t rank, int32_t world, const void *uid) 
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof id);
   SS_NCCL(c, ncclCommInitRank(&c->comm, world, id, rank));
+  uint64_t h = 1469598103934665603ull;  // FNV-1a of the unique id: the same tag on every rank of this job
+  for (size_t i = 0; i < sizeof id; ++i) h = (h ^ (uint8_t)id.internal[i]) * 1099511628211ull;
+  std::snprintf(c->job_tag, sizeof c->job_tag, "%016llx", (unsigned long long)h);
   c->rank = rank;
   c->world = world;
   c->L = ss::make_layout(c->P, c->S, c->n, rank, world);
@@ -707,6 +768,10 @@ void ss_destroy(ss_ctx *c) {
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   close_ipc(c, true);
+  if (c->w_vmm) {
+    c->w = nullptr;            // lives in the NVLS replica
+    ss::nvls_release(&c->nvls);
+  }
   if (c->comm) ncclCommDestroy(c->comm);
   for (float *p : c->stage) cudaFree(p);
   for (float *p : c->rslot) cudaFree(p);
@@ -834,7 +899,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
-  } else if (c->fused_mode != 0 && bsp_pipe_enabled()) {
+  } else if (c->fused_mode != 0 && bsp_pipe_enabled() && !c->nvls.ready) {
     // Fused peer-memory BSP, pipelined (experimental, SS_BSP_PIPE=1; kernels.cu pipe_bsp): one persistent kernel per rank.
     // Phase-A items store chunk slices of this rank's hosted gradients (mode 1) or of their ascending pre-sum (mode 2)
     // into the owners' inboxes and raise per-chunk flags; phase-B items reduce, update and broadcast each chunk of the
@@ -917,7 +982,10 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       sa.P = c->P;
       sa.sync = peer_sync(c, 0, epA, false);
       Timed t;
-      timed_begin(c, &t, 3, 4.0 * (double)c->P * (k + 1));
+      double remote = 0.0;
+      for (int32_t q = 0; q < c->world; ++q)
+        if (q != me) remote += (double)(c->real_hi[q] - c->real_lo[q]);
+      timed_begin(c, &t, 3, 4.0 * ((double)c->P * k + (double)(c->real_hi[me] - lo)), 4.0 * remote);
       SS_CUDA(c, ss::launch_scatter_sum(sa, c->stream));
       timed_end(c, &t);
     } else {
@@ -942,11 +1010,15 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     a.v = c->v;
     a.count = cnt;
     a.n_bcast = 0;
-    for (int32_t q = 0; q < c->world; ++q)
-      if (q != me) a.bcast[a.n_bcast++] = c->peer_w[q] + lo;
+    if (c->nvls.ready) {
+      a.mc_w = (float *)c->nvls.mcv + lo;   // NVLS: one multicast store per element reaches every replica
+    } else {
+      for (int32_t q = 0; q < c->world; ++q)
+        if (q != me) a.bcast[a.n_bcast++] = c->peer_w[q] + lo;
+    }
     a.sync = peer_sync(c, epA, epB, true);
     Timed t;
-    timed_begin(c, &t, 0, 4.0 * (double)cnt * (a.n_in + 4));
+    timed_begin(c, &t, 0, 4.0 * (double)cnt * (a.n_in + 4), 4.0 * (double)cnt * (c->nvls.ready ? 1 : a.n_bcast));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
   } else {
@@ -1176,12 +1248,14 @@ ss_status ss_profile(ss_ctx *c, int32_t on) {
   return SS_OK;
 }
 
-ss_status ss_kernel_stats(ss_ctx *c, int32_t id, int64_t *launches, double *ms, double *bytes) {
+ss_status ss_kernel_stats(ss_ctx *c, int32_t id, int64_t *launches, double *ms, double *bytes,
+                          double *nvlink_bytes) {
   if (!c || id < 0 || id > 3) return SS_E_INVAL;
   SS_TRY(drain_timed(c));
   if (launches) *launches = c->kstat[id].launches;
   if (ms) *ms = c->kstat[id].ms;
   if (bytes) *bytes = c->kstat[id].bytes;
+  if (nvlink_bytes) *nvlink_bytes = c->kstat[id].nvbytes;
   return SS_OK;
 }
 

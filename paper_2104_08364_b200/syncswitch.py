@@ -105,7 +105,7 @@ def _load():
         "ss_get_stream": [p, p],
         "ss_wait_stream": [p, p],
         "ss_profile": [p, i32],
-        "ss_kernel_stats": [p, i32, p, p, p],
+        "ss_kernel_stats": [p, i32, p, p, p, p],
         "ss_synth_grad": [u64, i32, i64, i64, i64, p, p],
         "ss_softmax_grad": [p, p, i32, i32, i32, p, p, p, p],
         "ss_dynamic_criterion": [p, p, i32, i32, i32, p, p, p, p, p],
@@ -286,9 +286,10 @@ def ss_profile(ctx, on: bool) -> int:
 
 
 def ss_kernel_stats(ctx, kernel_id: int):
-    n, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
-    ss_check(lib.ss_kernel_stats(ctx, kernel_id, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)), ctx)
-    return dict(launches=n.value, ms=ms.value, bytes=by.value)
+    n, ms, by, nv = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    ss_check(lib.ss_kernel_stats(ctx, kernel_id, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by),
+                                 ctypes.byref(nv)), ctx)
+    return dict(launches=n.value, ms=ms.value, bytes=by.value, nvlink_bytes=nv.value)
 
 
 def ss_destroy(ctx) -> None:
