@@ -522,33 +522,26 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int me = a.sync.rank;
-  const int64_t n4 = a.P >> 2, reg4 = a.reg_len >> 2;
-  constexpr int U = 4;
+  const int me = a.sync.rank, G = a.sync.world;
+  constexpr int U = 8;  // stores in flight per thread (posted NVLink writes; the loads come from local HBM)
   for (int k = 0; k < a.n_src; ++k) {
-    const float *src = a.src[k];
-    const int64_t slot_off = (int64_t)a.slot[k] * a.reg_len;
-    for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
-      float4 x[U];
+    for (int r = 0; r < G; ++r) {  // one contiguous segment per (source, destination rank): no per-element division
+      if (r == me) continue;
+      const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
+      const float *src = a.src[k] + lo;
+      float *dst = a.inbox[r] + (int64_t)a.slot[k] * a.reg_len;
+      const int64_t n4 = cnt >> 2;
+      for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+        float4 x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * stride;
-        if (q < n4 && q / reg4 != me) x[u] = ld4(src + 4 * q);
-      }
+        for (int u = 0; u < U; ++u)
+          if (q0 + u * stride < n4) x[u] = ld4(src + 4 * (q0 + u * stride));
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * stride;
-        if (q < n4) {
-          const int64_t r = q / reg4;
-          if (r != me)
-            *reinterpret_cast<float4 *>(a.inbox[r] + slot_off + 4 * (q - r * reg4)) = x[u];
-        }
+        for (int u = 0; u < U; ++u)
+          if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = x[u];
       }
-    }
-    const int64_t i = 4 * n4 + tid;  // scalar tail
-    if (i < a.P) {
-      const int64_t r = i / a.reg_len;
-      if (r != me) a.inbox[r][slot_off + (i - r * a.reg_len)] = src[i];
+      const int64_t i = 4 * n4 + tid;  // scalar tail
+      if (i < cnt) dst[i] = src[i];
     }
   }
   peer_done(a.sync);
