@@ -270,8 +270,8 @@ def run_ours(args):
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        h2d = 4 * P * 2 * len(hosted)
-        d2h = 4 * P * len(hosted)
+        h2d = 4 * P * 2 * n          # whole job: every worker's BSP and ASP gradient crosses PCIe once per step
+        d2h = 4 * P * n              # and every worker's pull snapshot comes back
         e2e = {"value": args.e2e_steps / (et.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "pinned host gradients and pull destinations, copies staged by the library"}
