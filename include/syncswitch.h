@@ -211,6 +211,20 @@ ss_status ss_set_window(ss_ctx *ctx, int32_t max_events);
 ss_status ss_get_stream(ss_ctx *ctx, void **stream_out);
 /* Order the context's work after `stream` (cudaStream_t) — used when gradients are produced on another stream. */
 ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
+/* CUDA-graph capture of one step (single GPU; SV §8(d): latency-bound small models "with and without CUDA Graphs").
+ * Between ss_capture_begin and ss_capture_end, the calls run their host logic as usual but their device work is
+ * recorded into a graph instead of executing; ss_capture_end instantiates it and launches it once (so the captured
+ * step has happened on both sides) and returns the step's version delta. ss_capture_replay(K) launches the graph K
+ * more times and applies the step's host-state deltas K times (versions, base versions, staleness histogram and
+ * log with shifted versions, dropped pushes). Replay requires the step to leave the protocol state as it found it
+ * (relative base versions, no pending switch, no queued window) and nothing baked into the kernels to change over
+ * the replayed versions (no lr boundary inside, momentum rule 0). Buffers the step used stay BORROWED while a
+ * graph exists. Calls that allocate (first use of host buffers) must not happen during capture: warm up first.
+ * Errors: SS_E_STATE, SS_E_CUDA. */
+ss_status ss_capture_begin(ss_ctx *ctx);
+ss_status ss_capture_end(ss_ctx *ctx, int64_t *version_delta);
+ss_status ss_capture_replay(ss_ctx *ctx, int64_t times);
+
 /* Kernel timing: when on, every launch of the path's kernels is bracketed by CUDA events on the context's stream;
  * ss_kernel_stats returns per-kernel launch count, total device milliseconds, algorithmic HBM bytes and algorithmic
  * bytes sent over NVLink by the fused multi-GPU path (kernel_id 0 = bsp_update, 1 = asp_replay, 2 = local_sum,

@@ -114,6 +114,12 @@ struct ss_ctx {
   char job_tag[48] = {0};              // names the NVLS fd socket: hash of the NCCL unique id + setup count
   uint32_t epoch = 0;
   int32_t first_hosted = 0, n_hosted = 0;
+  // CUDA-graph capture of one step (ss_capture_*): device work + the host-state deltas it produced
+  bool capturing = false;
+  cudaGraphExec_t graph = nullptr;
+  int64_t cap_v0 = 0, cap_dv = 0, cap_log0 = 0, cap_rel_since = 0;
+  uint64_t cap_ddropped = 0;
+  std::vector<int64_t> cap_base0, cap_log;   // log records appended during the captured step
   // instrumentation
   bool prof = false;
   std::vector<Timed> timed;
@@ -767,6 +773,7 @@ void ss_destroy(ss_ctx *c) {
     cudaEventDestroy(t.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
   close_ipc(c, true);
   if (c->w_vmm) {
     c->w = nullptr;            // lives in the NVLS replica
@@ -1140,7 +1147,86 @@ ss_status ss_asp_replay(ss_ctx *c, const ss_event *ev, int64_t n_ev, int64_t *st
 
 ss_status ss_sync(ss_ctx *c) {
   SS_TRY(check_live(c));
+  if (c->capturing) return fail(c, SS_E_STATE, "ss_sync inside a capture");
   return sync_impl(c);
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// CUDA-graph capture of one step (latency-bound small models). The device work the calls
+// between begin and end enqueue is recorded (not executed) into a graph; replay launches it K times and applies
+// the host-state deltas the step produced (versions, base versions, staleness records, drops) K times.
+ss_status ss_capture_begin(ss_ctx *c) {
+  SS_TRY(check_live(c));
+  if (c->world > 1) return fail(c, SS_E_STATE, "graph capture is single-GPU (the fused path's flag epochs change)");
+  if (c->capturing || c->prof) return fail(c, SS_E_STATE, "already capturing, or profiling is on");
+  SS_TRY(flush(c));
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  c->cap_v0 = c->version;
+  c->cap_base0 = c->base;
+  c->cap_log0 = (int64_t)c->log.size();
+  c->cap_ddropped = c->dropped;
+  c->cap_rel_since = c->version - c->asp_since;
+  SS_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
+  return SS_OK;
+}
+
+ss_status ss_capture_end(ss_ctx *c, int64_t *version_delta) {
+  if (!c || !c->capturing) return c ? fail(c, SS_E_STATE, "not capturing") : SS_E_INVAL;
+  ss_status fl = flush(c);   // every queued window joins the graph
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  c->capturing = false;
+  if (fl != SS_OK) return fl;
+  if (e != cudaSuccess) return fail(c, SS_E_CUDA, "capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(c, SS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  // the captured step already ran on the host side; its device work has not: run it once now
+  SS_CUDA(c, cudaGraphLaunch(c->graph, c->stream));
+  c->cap_dv = c->version - c->cap_v0;
+  c->cap_log.assign(c->log.begin() + c->cap_log0, c->log.end());
+  c->cap_ddropped = c->dropped - c->cap_ddropped;
+  if (version_delta) *version_delta = c->cap_dv;
+  return SS_OK;
+}
+
+ss_status ss_capture_replay(ss_ctx *c, int64_t times) {
+  SS_TRY(check_live(c));
+  if (!c->graph || times < 0) return fail(c, SS_E_STATE, "no captured step");
+  SS_TRY(maybe_switch(c));
+  // validity: the step must leave the protocol where it found it (relative base versions, no pending switch), and
+  // nothing the kernels baked in may change over the replayed versions (lr factor, momentum ramp)
+  const int64_t dv = c->cap_dv;
+  if (dv <= 0 || c->has_pending || c->win.size()) return fail(c, SS_E_STATE, "step not replayable");
+  for (int32_t j = 0; j < c->n; ++j)
+    if (c->base[j] - c->version != c->cap_base0[j] - c->cap_v0)
+      return fail(c, SS_E_STATE, "base versions do not shift uniformly");
+  const int64_t last = c->version + dv * times;
+  for (int64_t b : c->bounds)
+    if (b > c->cap_v0 && b < last) return fail(c, SS_E_STATE, "an lr boundary falls inside the replay");
+  if (c->mom_rule != 0) return fail(c, SS_E_STATE, "a momentum ramp changes inside the replay");
+  for (int64_t r = 0; r < times; ++r) {
+    SS_CUDA(c, cudaGraphLaunch(c->graph, c->stream));
+    const int64_t shift = c->version - c->cap_v0 - dv;   // version offset of this replay vs the captured step
+    for (size_t i = 0; i + 3 < c->cap_log.size(); i += 4) {
+      const int64_t st = c->cap_log[i + 2];
+      if ((size_t)st >= c->hist.size()) c->hist.resize((size_t)st + 1, 0);
+      c->hist[st] += 1;
+      c->log.push_back(c->cap_log[i]);
+      c->log.push_back(c->cap_log[i + 1] + shift + dv);
+      c->log.push_back(st);
+      c->log.push_back(c->cap_log[i + 3] + shift + dv);
+    }
+    c->version += dv;
+    for (auto &b : c->base) b += dv;
+    c->dropped += c->cap_ddropped;
+    if (c->asp_since >= c->cap_v0) c->asp_since += dv;   // the step switched to ASP: so does every replay
+  }
+  return SS_OK;
 }
 
 static ss_status gather_w(ss_ctx *c) {

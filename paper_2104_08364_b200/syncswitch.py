@@ -32,7 +32,8 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
            "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer",
            "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked",
-           "ss_dynamic_criterion", "ss_criterion_observe"]
+           "ss_dynamic_criterion", "ss_criterion_observe", "ss_capture_begin", "ss_capture_end",
+           "ss_capture_replay"]
 
 
 class SSError(RuntimeError):
@@ -102,6 +103,9 @@ def _load():
         "ss_get_stats": [p, p, p, p, i32, p],
         "ss_get_log": [p, p, i64, p],
         "ss_set_window": [p, i32],
+        "ss_capture_begin": [p],
+        "ss_capture_end": [p, p],
+        "ss_capture_replay": [p, i64],
         "ss_get_stream": [p, p],
         "ss_wait_stream": [p, p],
         "ss_profile": [p, i32],
@@ -521,6 +525,17 @@ class SyncSwitch:
 
     def log(self) -> np.ndarray:
         return ss_get_log(self.ctx)[1]
+
+    def capture_begin(self):
+        return self._chk(lib.ss_capture_begin(self.ctx))
+
+    def capture_end(self) -> int:
+        dv = ctypes.c_int64()
+        self._chk(lib.ss_capture_end(self.ctx, ctypes.byref(dv)))
+        return dv.value
+
+    def capture_replay(self, times: int):
+        return self._chk(lib.ss_capture_replay(self.ctx, times))
 
     def set_window(self, k: int):
         return self._chk(ss_set_window(self.ctx, k))

@@ -445,3 +445,55 @@ def test_momentum_policies_bit_exact(ss, orc, rule):
     g.sync()
     assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
     g.close()
+
+
+def test_graph_capture_replay_bit_exact(ss, orc):
+    """ss_capture_* (CUDA graph of one BSP + switch + ASP round + switch step, replayed K times) gives exactly the
+    protocol state and parameters of K + 1 ordinary steps (oracle)."""
+    n, S, P = 4, 4, 464154
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    g.set_window(2 * n)
+    bsp_g = [dev_synth(ss, j, 0, P) for j in range(n)]
+    asp_g = [dev_synth(ss, j, 1, P) for j in range(n)]
+    dst = [torch.empty(P, device="cuda") for _ in range(n)]
+    bsp_h = [host_synth(orc, j, 0, P) for j in range(n)]
+    asp_h = [host_synth(orc, j, 1, P) for j in range(n)]
+
+    def gpu_step():
+        v = g.version
+        g.bsp_step(bsp_g, list(range(n)), [v] * n)
+        g.switch(ASP, 0)
+        for j in range(n):
+            assert g.asp_push(j, asp_g[j], v + 1) == j
+            g.pull(j, dst[j])
+        g.switch(BSP, 0)
+
+    def orc_step():
+        v = o.version
+        assert o.bsp_step(bsp_h, versions=[v] * n) == 0
+        o.switch(ASP, 0)
+        for j in range(n):
+            assert o.asp_push(j, asp_h[j], v + 1) == (0, j)
+            o.pull(j, False)
+        o.switch(BSP, 0)
+
+    gpu_step()                      # warm-up (first use allocates nothing afterwards)
+    orc_step()
+    g.capture_begin()
+    gpu_step()
+    assert g.capture_end() == 1 + n
+    orc_step()
+    g.capture_replay(5)
+    for _ in range(5):
+        orc_step()
+    g.sync()
+    assert g.version == o.version == 7 * (1 + n)
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert np.array_equal(g.log(), o.log()) and np.array_equal(g.stats()["hist"], o.stats()["hist"])
+    assert np.array_equal(dst[n - 1].cpu().numpy(), o.params())
+    g.set_lr_schedule([100], [0.5])                 # a boundary inside the replay range is refused
+    with pytest.raises(ss.SSError):
+        g.capture_replay(20)
+    g.close()
