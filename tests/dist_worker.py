@@ -20,6 +20,11 @@ from paper_2104_08364_b200 import syncswitch as ss  # noqa: E402
 SEED = 20241018
 
 
+def sample_indices(P, count):
+    rng = np.random.default_rng(0)
+    return np.unique(np.concatenate([rng.choice(P, count - 4, replace=False), [0, 1, P - 2, P - 1]]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
@@ -33,6 +38,7 @@ def main():
     ap.add_argument("--fused", type=int, default=-1)
     ap.add_argument("--drop", type=int, default=-1, help="elastic: worker left out of --bsp-drop BSP steps")
     ap.add_argument("--bsp-drop", type=int, default=0)
+    ap.add_argument("--sample", type=int, default=0, help="save only this many sampled elements (full-size runs)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -97,9 +103,15 @@ def main():
     w = g.params()
     v = g.velocity()
     st = g.stats(64)
+    if a.sample:
+        idx = sample_indices(P, a.sample)
+        ti = torch.from_numpy(idx).cuda()
+        w, v = w[idx], v[idx]
+        snap_arr = np.stack([s[ti].cpu().numpy() for s in snaps]) if snaps else np.zeros((0, len(idx)), np.float32)
+    else:
+        snap_arr = np.stack([s.cpu().numpy() for s in snaps]) if snaps else np.zeros((0, P), np.float32)
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=w, v=v, stale=np.array(stale), log=g.log(),
-             hist=st["hist"], version=st["version"], dropped=st["dropped"],
-             snaps=np.stack([s.cpu().numpy() for s in snaps]) if snaps else np.zeros((0, P), np.float32),
+             hist=st["hist"], version=st["version"], dropped=st["dropped"], snaps=snap_arr,
              hosted=np.array(hosted))
     g.close()
     dist.barrier()

@@ -20,8 +20,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SEED = 20241018
 
 
-def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0):
-    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0, idx=None):
+    """The dist_worker call sequence on the oracle; with `idx`, on those elements only (elementwise update: exact for
+    them by shard invariance)."""
+    if idx is None:
+        w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    else:
+        w0 = np.array([orc.synth_grad(SEED + 1, 255, 0, int(i), 1)[0] for i in idx], np.float32) * np.float32(64.0)
+        S = 1
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
     o.set_lr_schedule([bsp1 + 10], [0.5])
     counter = {j: 0 for j in range(n)}
@@ -29,7 +35,9 @@ def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0):
     def grad(j):
         k = counter[j]
         counter[j] += 1
-        return orc.synth_grad(SEED, j, k, 0, P)
+        if idx is None:
+            return orc.synth_grad(SEED, j, k, 0, P)
+        return np.array([orc.synth_grad(SEED, j, k, int(i), 1)[0] for i in idx], np.float32)
 
     for _ in range(bsp1):
         assert o.bsp_step([grad(j) for j in range(n)]) == 0
@@ -111,3 +119,36 @@ def test_multi_gpu_parity(orc, world, case):
         assert len(exp) == len(r["snaps"]) == len(want)
         for a, b in zip(r["snaps"], exp):
             assert np.array_equal(a, b) if exact else close_c13(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [1, 2])
+def test_multi_gpu_full_size_sampled(orc, world, fused):
+    """Config 3 at full size (P = 25,557,032, n = S = 8, window 16: the bench's configuration) on `world` GPUs:
+    1 BSP superstep, a switch, 16 seeded ASP pushes with pulls, a switch back and 1 BSP superstep; 4,096 sampled
+    elements against the oracle (bit-exact in fused-exact mode, C13 in pre-summed mode), integers exact."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dist_worker import sample_indices
+    P, n, S = 25_557_032, 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 16, "--bsp1", 1, "--pushes", 16,
+                       "--bsp2", 1, "--fused", fused, "--sample", 4096], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    idx = sample_indices(P, 4096)
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 1, 16, 1, idx=idx)
+    exact = fused == 1
+    for r in res:
+        assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
+        cmp = np.array_equal if exact else close_c13
+        assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
+        hosted = [int(j) for j in r["hosted"]]
+        exp, cnt = [], {j: 0 for j in hosted}
+        for kd, j in zip(kind, worker):
+            if kd == 1 and int(j) in hosted:
+                exp.append(snaps[int(j)][cnt[int(j)]])
+                cnt[int(j)] += 1
+        assert len(exp) == len(r["snaps"])
+        for a, b in zip(r["snaps"], exp):
+            assert cmp(a, b)
