@@ -152,3 +152,35 @@ def test_multi_gpu_full_size_sampled(orc, world, fused):
         assert len(exp) == len(r["snaps"])
         for a, b in zip(r["snaps"], exp):
             assert cmp(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("shape", [(33, 3, 4), (1003, 6, 4), (97, 1, 4), (4099, 5, 8)])
+@pytest.mark.parametrize("fused", [0, 1, 2])
+def test_multi_gpu_edge_layouts(orc, world, shape, fused):
+    """Layouts the bench never uses: ranks hosting no worker (n < G), owner regions past the end of a tiny vector
+    (P = 33 on 4 ranks of 32-float shards), one worker for the whole job, n not a multiple of G; every exchange mode.
+    Protocol integers exact; parameters bit-exact (fused exact, pure ASP) or within C13 (NCCL / pre-summed BSP)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S = shape
+    if S % world:
+        pytest.skip("S must be a multiple of the world size")
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 5, "--bsp1", 2, "--pushes", 24,
+                       "--bsp2", 2, "--fused", fused], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 2, 24, 2)
+    cmp = np.array_equal if fused == 1 else close_c13
+    for r in res:
+        assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
+        assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
+        hosted = [int(j) for j in r["hosted"]]
+        exp, cnt = [], {j: 0 for j in hosted}
+        for kd, j in zip(kind, worker):
+            if kd == 1 and int(j) in hosted:
+                exp.append(snaps[int(j)][cnt[int(j)]])
+                cnt[int(j)] += 1
+        assert len(exp) == len(r["snaps"])
+        for a, b in zip(r["snaps"], exp):
+            assert cmp(a, b)
