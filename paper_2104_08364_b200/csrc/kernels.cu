@@ -525,8 +525,10 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
   const int me = a.sync.rank, G = a.sync.world;
   constexpr int U = 8;  // stores in flight per thread (posted NVLink writes; the loads come from local HBM)
   for (int k = 0; k < a.n_src; ++k) {
-    for (int r = 0; r < G; ++r) {  // one contiguous segment per (source, destination rank): no per-element division
-      if (r == me) continue;
+    // one contiguous segment per (source, destination rank), no per-element division; destinations in rotated order
+    // (me+1, me+2, ...) so that at any moment the ranks write to distinct receivers instead of all hitting one ingress
+    for (int step = 1; step < G; ++step) {
+      const int r = (me + step) % G;
       const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
       const float *src = a.src[k] + lo;
       float *dst = a.inbox[r] + (int64_t)a.slot[k] * a.reg_len;
@@ -552,44 +554,47 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n4 = a.P >> 2, reg4 = a.reg_len >> 2;
+  const int me = a.sync.rank, G = a.sync.world;
   const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
   constexpr int U = 2;
-  for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
-    float4 acc[U];
+  // destination regions in rotated order (me+1, ..., me): the ranks write to distinct receivers at any moment, and
+  // the own region (a local store) comes last
+  for (int step = 1; step <= G; ++step) {
+    const int r = (me + step) % G;
+    const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
+    float *dst = a.inbox[r] + slot_off;
+    const int64_t n4 = cnt >> 2;
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+      float4 acc[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * stride;
-      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (q < n4 && a.n_src > 0) acc[u] = ld4(a.src[0] + 4 * q);
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + u * stride;
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < n4 && a.n_src > 0) acc[u] = ld4(a.src[0] + lo + 4 * q);
+      }
+      for (int j0 = 1; j0 < a.n_src; j0 += kG1) {
+        float4 t[kG1][U];
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + jj < a.n_src && q0 + u * stride < n4) t[jj][u] = ld4(a.src[j0 + jj] + lo + 4 * (q0 + u * stride));
+#pragma unroll
+        for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + jj < a.n_src && q0 + u * stride < n4) acc[u] = add4(acc[u], t[jj][u]);  // ascending
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = acc[u];
     }
-    for (int j0 = 1; j0 < a.n_src; j0 += kG1) {
-      float4 t[kG1][U];
-#pragma unroll
-      for (int jj = 0; jj < kG1; ++jj)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j0 + jj < a.n_src && q0 + u * stride < n4) t[jj][u] = ld4(a.src[j0 + jj] + 4 * (q0 + u * stride));
-#pragma unroll
-      for (int jj = 0; jj < kG1; ++jj)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j0 + jj < a.n_src && q0 + u * stride < n4) acc[u] = add4(acc[u], t[jj][u]);
+    const int64_t i = 4 * n4 + tid;  // scalar tail of the segment
+    if (i < cnt) {
+      float acc = a.n_src > 0 ? a.src[0][lo + i] : 0.0f;
+      for (int k = 1; k < a.n_src; ++k) acc = __fadd_rn(acc, a.src[k][lo + i]);
+      dst[i] = acc;
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * stride;
-      if (q >= n4) continue;
-      const int64_t r = q / reg4;
-      *reinterpret_cast<float4 *>(a.inbox[r] + slot_off + 4 * (q - r * reg4)) = acc[u];
-    }
-  }
-  const int64_t i = 4 * n4 + tid;  // scalar tail
-  if (i < a.P) {
-    float acc = a.n_src > 0 ? a.src[0][i] : 0.0f;
-    for (int j = 1; j < a.n_src; ++j) acc = __fadd_rn(acc, a.src[j][i]);
-    const int64_t r = i / a.reg_len;
-    a.inbox[r][slot_off + (i - r * a.reg_len)] = acc;
   }
   peer_done(a.sync);
 }

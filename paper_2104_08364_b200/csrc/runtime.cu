@@ -1020,8 +1020,8 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     if (c->nvls.ready) {
       a.mc_w = (float *)c->nvls.mcv + lo;   // NVLS: one multicast store per element reaches every replica
     } else {
-      for (int32_t q = 0; q < c->world; ++q)
-        if (q != me) a.bcast[a.n_bcast++] = c->peer_w[q] + lo;
+      for (int32_t step = 1; step < c->world; ++step)   // rotated: the ranks' stores go to distinct receivers
+        a.bcast[a.n_bcast++] = c->peer_w[(me + step) % c->world] + lo;
     }
     a.sync = peer_sync(c, epA, epB, true);
     Timed t;
