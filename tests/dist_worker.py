@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--drop", type=int, default=-1, help="elastic: worker left out of --bsp-drop BSP steps")
     ap.add_argument("--bsp-drop", type=int, default=0)
     ap.add_argument("--sample", type=int, default=0, help="save only this many sampled elements (full-size runs)")
+    ap.add_argument("--host-buffers", type=int, default=0, help="gradients and pull destinations in host memory")
+    ap.add_argument("--scenario", type=int, default=-1, help="run ss_scenario_run with this policy instead")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -69,8 +71,27 @@ def main():
             return None
         buf = torch.empty(P, device="cuda")
         ss.ss_check(ss.ss_synth_grad(SEED, j, k, 0, P, buf))
+        if a.host_buffers:                 # the e2e path: pinned host memory, staged by the library
+            torch.cuda.synchronize()
+            buf = buf.cpu().pin_memory()
         keep.append(buf)
         return buf
+
+    if a.scenario >= 0:
+        sc = dict(n_workers=n, batch=128, total_samples=600 * 128, quota_num=1, quota_den=2, period=1000, jitter=0,
+                  sched_seed=7, grad_seed=SEED, slow_worker=n - 1, slow_factor=4, slow_t0=3000, slow_t1=30000,
+                  window_ticks=4000, K=2, policy=a.scenario)
+        s_, log, res = ss.ss_scenario_run(g.ctx, sc)
+        ss.ss_check(s_, g.ctx)
+        g.sync()
+        st = g.stats(64)
+        np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=g.params(), v=g.velocity(), log=np.array(log),
+                 res=np.array([res[k] for k in ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version")]),
+                 hist=st["hist"], plog=g.log())
+        g.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
 
     for _ in range(a.bsp1):
         gs = {j: grad(j) for j in range(n)}
@@ -89,7 +110,9 @@ def main():
     for kd, j in zip(kind, worker):
         j = int(j)
         if kd == 1:
-            dst = torch.empty(P, device="cuda") if j in hosted else None
+            dst = None
+            if j in hosted:
+                dst = torch.empty(P, pin_memory=True) if a.host_buffers else torch.empty(P, device="cuda")
             base[j] = g.pull(j, dst)
             if dst is not None:
                 snaps.append(dst)
@@ -109,7 +132,7 @@ def main():
         w, v = w[idx], v[idx]
         snap_arr = np.stack([s[ti].cpu().numpy() for s in snaps]) if snaps else np.zeros((0, len(idx)), np.float32)
     else:
-        snap_arr = np.stack([s.cpu().numpy() for s in snaps]) if snaps else np.zeros((0, P), np.float32)
+        snap_arr = np.stack([s.cpu().numpy().copy() for s in snaps]) if snaps else np.zeros((0, P), np.float32)
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=w, v=v, stale=np.array(stale), log=g.log(),
              hist=st["hist"], version=st["version"], dropped=st["dropped"], snaps=snap_arr,
              hosted=np.array(hosted))

@@ -184,3 +184,57 @@ def test_multi_gpu_edge_layouts(orc, world, shape, fused):
         assert len(exp) == len(r["snaps"])
         for a, b in zip(r["snaps"], exp):
             assert cmp(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [0, 1])
+def test_multi_gpu_host_buffers(orc, world, fused):
+    """The e2e path at G > 1: gradients and pull destinations in pinned host memory (staged by the library) —
+    same results as device buffers (bit-exact in fused-exact mode)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S = 10007, 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 7, "--bsp1", 2, "--pushes", 30,
+                       "--bsp2", 1, "--fused", fused, "--host-buffers", 1], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 2, 30, 1)
+    cmp = np.array_equal if fused == 1 else close_c13
+    for r in res:
+        assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
+        assert cmp(r["w"], o.params())
+        hosted = [int(j) for j in r["hosted"]]
+        exp, cnt = [], {j: 0 for j in hosted}
+        for kd, j in zip(kind, worker):
+            if kd == 1 and int(j) in hosted:
+                exp.append(snaps[int(j)][cnt[int(j)]])
+                cnt[int(j)] += 1
+        for a, b in zip(r["snaps"], exp):
+            assert cmp(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_multi_gpu_scenario(orc, world, policy):
+    """The config-4 scenario runner (greedy / elastic) across `world` GPUs (fused exact): the same switch log and
+    results as the oracle's run, bit-exact parameters."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S = 4099, 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 16, "--fused", 1, "--bsp1", 0,
+                       "--scenario", policy], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    sc = dict(n_workers=n, batch=128, total_samples=600 * 128, quota_num=1, quota_den=2, period=1000, jitter=0,
+              sched_seed=7, grad_seed=SEED, slow_worker=n - 1, slow_factor=4, slow_t0=3000, slow_t1=30000,
+              window_ticks=4000, K=2, policy=policy)
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    o.set_lr_schedule([10], [0.5])
+    log, out = orc.scenario(sc, o, P)
+    assert len(log) >= 2                               # the straggler triggered the policy
+    for r in res:
+        assert [tuple(int(x) for x in e) for e in r["log"]] == log
+        assert list(r["res"]) == [out[k] for k in ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version")]
+        assert np.array_equal(r["plog"], o.log()) and np.array_equal(r["hist"], o.stats(64)["hist"])
+        assert np.array_equal(r["w"], o.params()) and np.array_equal(r["v"], o.velocity())
