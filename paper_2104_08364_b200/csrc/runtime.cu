@@ -33,6 +33,7 @@ struct Ev {
                         //       nullptr on ranks not hosting the worker
   float *dst;           // pull: device destination (full length) on the hosting rank, else nullptr
   float *host_dst;      // pull into host memory: D2H from dst after the window
+  int32_t slot = -1;    // staging slot behind dst (host destination), or -1
   float lr;             // push: eta_ASP at the push's (pre-increment) version
   float mu;             // push: momentum (post-switch momentum policy)
   bool data;            // pull: moves parameters (false: version-only pull, G = 1)
@@ -82,6 +83,11 @@ struct ss_ctx {
   float *rs_buf = nullptr;             // G > 1: reduce-scattered sum [reg_len]
   std::vector<float *> stage;          // full-length staging slots for host pointers
   int32_t stage_used = 0;
+  // single GPU: host<->device staging copies run on their own streams so PCIe traffic in both directions overlaps
+  // the kernels and each other; per-slot events order reuse (slot_free) and consumption (slot_ready)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> slot_free, slot_ready;
+  std::vector<uint8_t> slot_armed;     // slot_free has been recorded at least once
   std::vector<float *> rslot, sslot;   // G > 1: received gradient shards / snapshot shards per window event
   // protocol state (host; bit-exact with the oracle)
   int64_t version = 0;
@@ -217,26 +223,71 @@ void record(ss_ctx *c, int64_t worker, int64_t b, int64_t st) {
   c->log.push_back(c->version);
 }
 
-ss_status stage_slot(ss_ctx *c, float **out) {
+ss_status stage_slot(ss_ctx *c, float **out, int32_t *index = nullptr) {
+  if (c->capturing) return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
   if (c->stage_used == (int32_t)c->stage.size()) {
     float *p = nullptr;
+    cudaEvent_t f, r;
     SS_CUDA(c, cudaMalloc(&p, (size_t)c->P_pad * sizeof(float)));
+    SS_CUDA(c, cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
+    SS_CUDA(c, cudaEventCreateWithFlags(&r, cudaEventDisableTiming));
     c->stage.push_back(p);
+    c->slot_free.push_back(f);
+    c->slot_ready.push_back(r);
+    c->slot_armed.push_back(0);
   }
+  if (index) *index = c->stage_used;
   *out = c->stage[c->stage_used++];
   return SS_OK;
 }
 
-// Host gradient -> device staging slot (stream-ordered; the caller's buffer is borrowed until ss_sync).
+bool split_copies(const ss_ctx *c) { return c->world == 1 && c->copy_in != nullptr; }
+
+// Host gradient -> device staging slot (the caller's buffer is borrowed until ss_sync). Single GPU: the H2D runs on
+// copy_in after the slot's previous consumer, and the compute stream waits only for this copy.
 ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
   if (!is_host_ptr(g)) {
     *out = g;
     return SS_OK;
   }
   float *slot = nullptr;
-  SS_TRY(stage_slot(c, &slot));
-  SS_CUDA(c, cudaMemcpyAsync(slot, g, (size_t)c->P * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  int32_t i = 0;
+  SS_TRY(stage_slot(c, &slot, &i));
+  if (split_copies(c)) {
+    if (c->slot_armed[i]) SS_CUDA(c, cudaStreamWaitEvent(c->copy_in, c->slot_free[i], 0));
+    SS_CUDA(c, cudaMemcpyAsync(slot, g, (size_t)c->P * sizeof(float), cudaMemcpyHostToDevice, c->copy_in));
+    SS_CUDA(c, cudaEventRecord(c->slot_ready[i], c->copy_in));
+    SS_CUDA(c, cudaStreamWaitEvent(c->stream, c->slot_ready[i], 0));
+  } else {
+    SS_CUDA(c, cudaMemcpyAsync(slot, g, (size_t)c->P * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
   *out = slot;
+  return SS_OK;
+}
+
+// After the kernel that consumed slots [0, stage_used) was enqueued: they may be refilled once it is done.
+ss_status release_slots(ss_ctx *c) {
+  if (split_copies(c))
+    for (int32_t i = 0; i < c->stage_used; ++i) {
+      SS_CUDA(c, cudaEventRecord(c->slot_free[i], c->stream));
+      c->slot_armed[i] = 1;
+    }
+  c->stage_used = 0;
+  return SS_OK;
+}
+
+// A pull into host memory: D2H from its staging slot on copy_out once the window's kernel wrote it; the slot is free
+// again when the copy is done.
+ss_status pull_to_host(ss_ctx *c, const Ev &e) {
+  if (!split_copies(c) || e.slot < 0) {
+    SS_CUDA(c, cudaMemcpyAsync(e.host_dst, e.dst, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    return SS_OK;
+  }
+  SS_CUDA(c, cudaEventRecord(c->slot_ready[e.slot], c->stream));
+  SS_CUDA(c, cudaStreamWaitEvent(c->copy_out, c->slot_ready[e.slot], 0));
+  SS_CUDA(c, cudaMemcpyAsync(e.host_dst, e.dst, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->copy_out));
+  SS_CUDA(c, cudaEventRecord(c->slot_free[e.slot], c->copy_out));
+  c->slot_armed[e.slot] = 1;
   return SS_OK;
 }
 
@@ -614,10 +665,19 @@ ss_status flush(ss_ctx *c) {
     SS_NCCL(c, ncclGroupEnd());
   }
 
+  // slots read by the kernel (gradients) are free after it; host pulls free theirs after their D2H
+  if (split_copies(c)) {
+    std::vector<uint8_t> is_pull(c->stage_used, 0);
+    for (const Ev &e : c->win)
+      if (e.kind == 1 && e.host_dst && e.slot >= 0) is_pull[e.slot] = 1;
+    for (int32_t i = 0; i < c->stage_used; ++i)
+      if (!is_pull[i]) {
+        SS_CUDA(c, cudaEventRecord(c->slot_free[i], c->stream));
+        c->slot_armed[i] = 1;
+      }
+  }
   for (const Ev &e : c->win)
-    if (e.kind == 1 && e.host_dst)
-      SS_CUDA(c, cudaMemcpyAsync(e.host_dst, e.dst, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost,
-                                 c->stream));
+    if (e.kind == 1 && e.host_dst) SS_TRY(pull_to_host(c, e));
   c->win.clear();
   c->stage_used = 0;
   return SS_OK;
@@ -663,6 +723,8 @@ ss_status enqueue(ss_ctx *c, const Ev &e) {
 ss_status sync_impl(ss_ctx *c) {
   SS_TRY(flush(c));
   SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->copy_in) SS_CUDA(c, cudaStreamSynchronize(c->copy_in));
+  if (c->copy_out) SS_CUDA(c, cudaStreamSynchronize(c->copy_out));
   int h = 0;
   SS_CUDA(c, cudaMemcpy(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) c->diverged = true;
@@ -711,6 +773,9 @@ ss_status ss_init(ss_ctx **out, const float *params, int64_t n_params, int32_t n
   };
   if (cudaGetDevice(&c->device) != cudaSuccess) return bail(SS_E_CUDA);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SS_E_CUDA);
+  if (cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(SS_E_CUDA);
   if (cudaMalloc(&c->w, (size_t)c->P_pad * sizeof(float)) != cudaSuccess) return bail(SS_E_OOM);
   if (cudaMalloc(&c->v, (size_t)c->P_pad * sizeof(float)) != cudaSuccess) return bail(SS_E_OOM);
   if (cudaMalloc(&c->flag, sizeof(int)) != cudaSuccess) return bail(SS_E_OOM);
@@ -780,7 +845,13 @@ void ss_destroy(ss_ctx *c) {
     ss::nvls_release(&c->nvls);
   }
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->copy_in) cudaStreamSynchronize(c->copy_in);
+  if (c->copy_out) cudaStreamSynchronize(c->copy_out);
   for (float *p : c->stage) cudaFree(p);
+  for (cudaEvent_t e : c->slot_free) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->slot_ready) cudaEventDestroy(e);
+  if (c->copy_in) cudaStreamDestroy(c->copy_in);
+  if (c->copy_out) cudaStreamDestroy(c->copy_out);
   for (float *p : c->rslot) cudaFree(p);
   for (float *p : c->sslot) cudaFree(p);
   cudaFree(c->sum_buf);
@@ -1060,7 +1131,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     SS_NCCL(c, ncclAllGather(c->w + (int64_t)c->rank * c->reg_len, c->w, c->reg_len, ncclFloat, c->comm,
                              c->stream));
   }
-  c->stage_used = 0;
+  SS_TRY(release_slots(c));
   for (int32_t j = 0; j < c->n; ++j)
     if (c->member[j]) record(c, j, c->version, 0);  // one staleness-0 record per BSP member
   c->version += 1;
@@ -1112,7 +1183,7 @@ ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
   if (mine) {
     if (is_host_ptr(dst)) {
       float *slot = nullptr;
-      SS_TRY(stage_slot(c, &slot));
+      SS_TRY(stage_slot(c, &slot, &e.slot));
       e.dst = slot;
       e.host_dst = dst;
     } else {

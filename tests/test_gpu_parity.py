@@ -141,10 +141,12 @@ def test_asp_bit_exact(ss, orc, window, P, S):
     g.close()
 
 
-def test_asp_host_buffers_and_weight_decay(ss, orc):
+@pytest.mark.parametrize("window", [2, 16])
+def test_asp_host_buffers_and_weight_decay(ss, orc, window):
+    # host gradients and pull destinations: staged on the copy streams (H2D / D2H overlapping the kernels)
     n, P = 3, 3001
     kind, worker, _ = orc.schedule(n, [1000] * n, 40, jitter=100, seed=3)
-    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, 2, kind, worker, 16, host_buffers=True, lam=1e-3)
+    g, o, pg, po, sg, so = run_asp_pair(ss, orc, P, n, 2, kind, worker, window, host_buffers=True, lam=1e-3)
     assert sg == so
     for a, b in zip(pg, po):
         assert np.array_equal(a, b)
@@ -503,4 +505,30 @@ def test_graph_capture_replay_bit_exact(ss, orc):
     g.set_lr_schedule([100], [0.5])                 # a boundary inside the replay range is refused
     with pytest.raises(ss.SSError):
         g.capture_replay(20)
+    g.close()
+
+
+def test_bsp_host_gradients_reuse_slots(ss, orc):
+    """BSP supersteps from host gradients, twice per slot set, then an ASP round with host pulls: the copy streams
+    must respect slot reuse (a refill waits for the previous consumer)."""
+    n, S, P = 4, 2, 70001
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for step in range(4):
+        hg = [host_synth(orc, j, step, P) for j in range(n)]
+        g.bsp_step(hg)                                   # no sync between steps: staging slots are reused
+        assert o.bsp_step(hg) == 0
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    g.set_window(2)
+    outs = [np.empty(P, np.float32) for _ in range(n)]
+    for j in range(n):
+        hg = host_synth(orc, j, 9, P)
+        g.asp_push(j, hg, 4)
+        o.asp_push(j, hg, 4)
+        g.pull(j, outs[j])
+    g.sync()
+    assert np.array_equal(g.params(), o.params())
+    assert np.array_equal(outs[n - 1], o.params())
     g.close()
