@@ -68,7 +68,8 @@ def test_bsp_bit_exact(ss, orc, P, n, S, lam):
     w0 = init_params(orc, P)
     g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.05, 0.9)
     o = orc.Oracle(w0, S, n, 0.05, 0.9)
-    for x in (g, o):
+    o64 = orc.Oracle(w0, S, n, 0.05, 0.9, dtype=np.float64)    # the fp64 reference of the same method
+    for x in (g, o, o64):
         x.set_lr_schedule([2], [0.1])        # a decay boundary inside the run (version coordinate)
         x.set_lr_policy(0, lam)
     for step in range(3):
@@ -77,8 +78,10 @@ def test_bsp_bit_exact(ss, orc, P, n, S, lam):
         perm = list(reversed(range(n)))       # order of submission must not matter (sum is ascending by id)
         g.bsp_step([dg[j] for j in perm], perm, [step] * n)
         assert o.bsp_step(hg) == 0
-    assert np.array_equal(g.params(), o.params())
+        assert o64.bsp_step([h.astype(np.float64) for h in hg]) == 0
+    assert np.array_equal(g.params(), o.params())          # bit-exact with the same-precision oracle (C12)
     assert np.array_equal(g.velocity(), o.velocity())
+    assert close_c13(g.params(), o64.params()) and close_c13(g.velocity(), o64.velocity())   # <= 1e-5 of fp64
     sg, so = g.stats(), o.stats()
     assert sg["version"] == so["version"] == 3 and np.array_equal(sg["hist"], so["hist"])
     assert np.array_equal(g.log(), o.log())
@@ -90,7 +93,8 @@ def run_asp_pair(ss, orc, P, n, S, kind, worker, window, host_buffers=False, off
     w0 = init_params(orc, P)
     g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
-    for x in (g, o):
+    o64 = orc.Oracle(w0, S, n, 0.1, 0.9, dtype=np.float64)
+    for x in (g, o, o64):
         x.set_lr_schedule([60], [0.5])
         x.set_lr_policy(0, lam)
         x.switch(ASP, 0)
@@ -122,7 +126,9 @@ def run_asp_pair(ss, orc, P, n, S, kind, worker, window, host_buffers=False, off
             rc, s = o.asp_push(j, host_synth(orc, j, k, P), base_o[j])
             assert rc == 0
             st_o.append(s)
+            assert o64.asp_push(j, host_synth(orc, j, k, P).astype(np.float64), base_o[j])[0] == 0
     g.sync()
+    assert close_c13(g.params(), o64.params())           # within the north-star tolerance of the fp64 result
     return g, o, pulls_g, pulls_o, st_g, st_o
 
 
@@ -531,4 +537,19 @@ def test_bsp_host_gradients_reuse_slots(ss, orc):
     g.sync()
     assert np.array_equal(g.params(), o.params())
     assert np.array_equal(outs[n - 1], o.params())
+    g.close()
+
+
+def test_max_workers_bsp(ss, orc):
+    """The maximum cluster the C-ABI accepts (n = 256 workers in one superstep, S = 64 shards)."""
+    n, S, P = 256, 64, 20011
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.001, 0.9)
+    o = orc.Oracle(w0, S, n, 0.001, 0.9)
+    for step in range(2):
+        dg = [dev_synth(ss, j, step, P) for j in range(n)]
+        g.bsp_step(dg)
+        assert o.bsp_step([host_synth(orc, j, step, P) for j in range(n)]) == 0
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert g.stats(2)["hist"][0] == 2 * n
     g.close()
