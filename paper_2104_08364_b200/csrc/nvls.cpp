@@ -9,6 +9,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <poll.h>
 #include <sys/socket.h>
 #include <sys/un.h>
 #include <unistd.h>
@@ -124,10 +125,10 @@ bool nvls_supported(int device) {
   return v != 0;
 }
 
-// Collective over `world` processes. Step 1 (rank 0) creates the object and serves its fd; step 2 every rank imports
-// it and adds its device; step 3 every rank binds fresh device memory and maps both the unicast and the multicast
-// view. The caller separates steps with a barrier; `tag` names the socket (unique per job and setup).
-const char *nvls_setup(NvlsReplica *r, int rank, int world, int device, size_t bytes, const char *tag) {
+// Phase 1, collective over `world` processes: rank 0 creates the object and serves its fd (every wait bounded by 60 s);
+// every rank imports it and adds its device. The caller must agree on success across ranks before phase 2, because
+// binding blocks until every device has been added. `tag` names the socket (unique per job).
+const char *nvls_share(NvlsReplica *r, int rank, int world, int device, size_t bytes, const char *tag) {
   Drv &d = drv();
   if (!d.ok) return "driver multicast entry points unavailable";
   CUdevice dev;
@@ -157,6 +158,12 @@ const char *nvls_setup(NvlsReplica *r, int rank, int world, int device, size_t b
       return "unix socket bind/listen failed";
     }
     for (int i = 1; i < world; ++i) {
+      pollfd pf{srv, POLLIN, 0};
+      if (poll(&pf, 1, 60000) != 1) {   // a peer that never connects must not hang rank 0
+        close(srv);
+        close(fd);
+        return "no connection from a peer within 60 s";
+      }
       const int cl = accept(srv, nullptr, nullptr);
       if (cl < 0 || !send_fd(cl, fd)) {
         if (cl >= 0) close(cl);
@@ -187,7 +194,16 @@ const char *nvls_setup(NvlsReplica *r, int rank, int world, int device, size_t b
     if (e != CUDA_SUCCESS) return "cuMemImportFromShareableHandle failed";
   }
   if (d.MulticastAddDevice(r->mc, dev) != CUDA_SUCCESS) return "cuMulticastAddDevice failed";
+  r->device = device;
+  r->gran = gran;
+  return nullptr;
+}
 
+// Phase 2 (after every rank's phase 1 succeeded): bind fresh device memory and map the unicast and multicast views.
+const char *nvls_bind(NvlsReplica *r) {
+  Drv &d = drv();
+  const size_t size = r->size, gran = r->gran;
+  const int device = r->device;
   CUmemAllocationProp ap{};
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -198,7 +214,6 @@ const char *nvls_setup(NvlsReplica *r, int rank, int world, int device, size_t b
   // blocks until every rank has added its device
   if (d.MulticastBindMem(r->mc, 0, r->mem, 0, size, 0) != CUDA_SUCCESS) return "cuMulticastBindMem failed";
   r->bound = true;
-  r->device = device;
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = device;

@@ -393,10 +393,15 @@ ss_status ensure_nvls(ss_ctx *c) {
   int32_t ok = want && ss::nvls_supported(c->device) ? 1 : 0;
   SS_TRY(agree_all(c, &ok));
   if (!ok) return SS_OK;
-  const char *why = ss::nvls_setup(&c->nvls, c->rank, c->world, c->device, (size_t)c->P_pad * sizeof(float),
+  const char *why = ss::nvls_share(&c->nvls, c->rank, c->world, c->device, (size_t)c->P_pad * sizeof(float),
                                    c->job_tag);
   ok = why == nullptr;
-  SS_TRY(agree_all(c, &ok));
+  SS_TRY(agree_all(c, &ok));   // binding blocks until every rank added its device: bind only if all of them did
+  if (ok) {
+    why = ss::nvls_bind(&c->nvls);
+    ok = why == nullptr;
+    SS_TRY(agree_all(c, &ok));
+  }
   if (!ok) {
     if (why) fprintf(stderr, "syncswitch: NVLS multicast unavailable on rank %d (%s); using P2P stores\n", c->rank,
                      why);
