@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <mutex>
 #include <unordered_map>
 
 #include "internal.h"
@@ -924,6 +925,8 @@ int num_sms() {
 template <typename K>
 int resident_ctas(K kernel) {
   static std::unordered_map<const void *, int> cache;
+  static std::mutex mu;                       // contexts may live on different threads
+  std::lock_guard<std::mutex> lock(mu);
   const void *key = reinterpret_cast<const void *>(kernel);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
