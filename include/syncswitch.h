@@ -141,14 +141,18 @@ ss_status ss_current_lr(ss_ctx *ctx, int32_t protocol, float *lr_out);
  * ============================================================================================================ */
 
 /* BSP superstep (Fig. 3: gradients are aggregated at a barrier, then the model is updated).
- *   grads[i]    host or device fp32[n_params]: the gradient of worker workers[i] (BORROWED until ss_sync).
+ *   grads[i]    host or device fp32[n_params]: the gradient of worker workers[i] (BORROWED until ss_sync; host
+ *               memory is staged on a copy stream). Device pointers should be 16-byte aligned (the fused multi-GPU
+ *               path requires it; single GPU falls back to a scalar kernel otherwise).
  *   versions[i] the base version that gradient was computed on; must equal the current version.
- *   n_local     number of gradients supplied. Single GPU: exactly the n workers, each once. Multi-GPU: exactly
- *               the workers hosted on this rank.
- * Computes g = (sum_{j ascending} g_j) / n (+ lambda*w), v = mu*v + g, w = w - eta_BSP*v over every shard
- * (kernel bsp_update; G > 1: local sum -> NCCL reduce-scatter -> owner update -> NCCL all-gather), then
- * version += 1 and every worker's base version = version; n staleness-0 records.
- * Errors: SS_E_STATE (protocol is ASP), SS_E_PROTOCOL (missing/duplicate worker), SS_E_BARRIER, SS_E_INVAL. */
+ *   n_local     number of gradients supplied: exactly the BSP members (all n unless ss_set_members shrank the
+ *               set), each once; multi-GPU: exactly the members hosted on this rank.
+ * Computes g = (sum_{members, ascending} g_j) / m (+ lambda*w), v = mu*v + g, w = w - eta_BSP*v over every shard
+ * (m = number of members; kernel bsp_update; G > 1 per ss_set_fused: NCCL reduce-scatter / all-gather, or the
+ * fused peer-memory scatter -> owner update -> broadcast), then version += 1 and every worker's base version =
+ * version; one staleness-0 record per member.
+ * Errors: SS_E_STATE (protocol is ASP), SS_E_PROTOCOL (missing/duplicate/non-member worker), SS_E_BARRIER,
+ * SS_E_INVAL. */
 ss_status ss_bsp_step(ss_ctx *ctx, const float *const *grads, const int32_t *workers, const int64_t *versions,
                       int32_t n_local);
 
@@ -156,14 +160,16 @@ ss_status ss_bsp_step(ss_ctx *ctx, const float *const *grads, const int32_t *wor
  * `worker`, BORROWED until ss_sync (multi-GPU: non-NULL only on the rank hosting `worker`; NULL elsewhere).
  * version: the worker's base version (from its last ss_pull). Returns *staleness_out = current - version
  * immediately, then version += 1. The update itself is applied by the asp_replay kernel when the
- * window is flushed (window full, ss_pull with a pending window, ss_sync, ss_switch, ss_bsp_step, ss_read_params).
+ * replay window is flushed: when it holds ss_set_window events (pushes and pulls count), or at ss_sync,
+ * ss_read_params, a switch taking effect, ss_bsp_step, ss_set_window/ss_set_fused/ss_set_lr_policy, capture end.
  * Errors: SS_E_STATE (protocol is BSP; counted in dropped_pushes), SS_E_CAUSALITY, SS_E_INVAL. */
 ss_status ss_asp_push(ss_ctx *ctx, int32_t worker, const float *grad, int64_t version, int64_t *staleness_out);
 
 /* Pull ("a worker will first pull model parameters from all PSs"). dst: host or device fp32[n_params]
- * (BORROWED until ss_sync; NULL = version only; multi-GPU: non-NULL only on the rank hosting `worker`). Receives
- * the parameters after exactly the pushes that precede this call, valid after ss_sync. *version_out = current
- * version; it becomes the worker's base version. Errors: SS_E_INVAL. */
+ * (BORROWED until ss_sync). NULL = version only (single GPU); multi-GPU: every pull moves data, so dst must be
+ * non-NULL on the rank hosting `worker` and NULL elsewhere. A pull is an event of the replay window: dst receives the
+ * parameters after exactly the pushes that precede this call (on every shard), valid after ss_sync. *version_out =
+ * current version; it becomes the worker's base version. Errors: SS_E_INVAL. */
 ss_status ss_pull(ss_ctx *ctx, int32_t worker, float *dst, int64_t *version_out);
 
 /* Switch to `protocol` when the version reaches at_step (at_step <= current: now). w, v and version are carried
@@ -184,7 +190,8 @@ typedef struct {
 } ss_event;
 ss_status ss_asp_replay(ss_ctx *ctx, const ss_event *ev, int64_t n_ev, int64_t *staleness_out);
 
-/* Flush pending windows, wait for the context's stream, surface asynchronous errors (SS_E_DIVERGED, SS_E_CUDA). */
+/* Flush the pending window, wait for the context's streams, surface asynchronous errors (SS_E_DIVERGED; SS_E_CUDA,
+ * including a fused-path cross-GPU wait that timed out). Not allowed while capturing a graph (SS_E_STATE). */
 ss_status ss_sync(ss_ctx *ctx);
 
 /* Copies the unpadded parameters w (fp32[n_params]) / momentum v to a HOST buffer (collective when distributed).
