@@ -13,7 +13,8 @@
  *    final when the call returns. Device data movement is stream-ordered on the context's stream and may be
  *    batched lazily (ASP windows); it is complete after ss_sync().
  *  - Pointers documented "host or device" may point to device memory (cudaMalloc / torch CUDA tensors), pinned or
- *    pageable host memory; host data is staged through device buffers with copies on the context's stream.
+ *    pageable host memory; host data is staged through device buffers (single GPU: on dedicated H2D / D2H copy
+ *    streams ordered by events, so transfers in both directions overlap the kernels).
  *  - Buffers passed to a call are BORROWED until the next ss_sync() returns (the library may read/write them
  *    lazily); params passed to ss_init are COPIED. The caller keeps ownership of every buffer it passes.
  *  - A context is not thread-safe: one thread per context, calls in program order.
@@ -85,7 +86,9 @@ ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *ncc
  *      hang). At most 8 ranks.
  *   2  fused peer memory, pre-summed: as 1, but each rank first sums its hosted workers and sends one slice per
  *      owner (fewer NVLink bytes when n > world; summation order: ascending within a rank, then ascending ranks).
- * Errors: SS_E_INVAL. */
+ * In modes 1 and 2 the BSP broadcast of the updated slices uses NVSwitch multicast (NVLS, one multimem.st per
+ * element reaches every replica) when world >= 8 and the driver supports it, else P2P stores; environment variable
+ * SS_NVLS=0/1 overrides. Errors: SS_E_INVAL. */
 ss_status ss_set_fused(ss_ctx *ctx, int32_t mode);
 
 /* Fused multi-GPU mode: the CUDA-IPC-mapped pull buffer (device fp32[P_pad], owned by the context, valid until
