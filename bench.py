@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fused", default="auto", choices=["auto", "0", "1", "2"],
                     help="G>1 exchange: 0 NCCL, 1 fused exact, 2 fused pre-summed; auto = 1 if n <= G else 2")
+    ap.add_argument("--workload", action="store_true",
+                    help="config 2/3: sync-only time of the whole 64K-iteration workload, pure BSP / pure ASP / "
+                         "switched (Table I remap)")
+    ap.add_argument("--window", type=int, default=0, help="ASP replay window in events (0: the config's default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -145,7 +149,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
-    P, n, S, win = cfg["P"], cfg["n"], cfg["S"], cfg["window"]
+    P, n, S, win = cfg["P"], cfg["n"], cfg["S"], args.window or cfg["window"]
     hosted = [j for j in range(n) if (j * world) // n == rank]
 
     # initial parameters (seeded, identical on every rank) and the context
@@ -410,6 +414,168 @@ def run_scenario(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------------------------------------
+# --workload: sync-only time of the whole 64K-iteration training workload (the sync-path
+# analog of Table II's throughput column): pure BSP, pure ASP and switched at s, each with the Table I
+# workload-preserving remap of steps and lr-decay boundaries (DESIGN reading C11).
+WORKLOADS = {
+    # W samples, B per worker, switch point s = num/den of W (P:1552 for config 3's 12.5%), decay boundaries W_i in
+    # samples with their factors (config 2: ResNet-32 on CIFAR-10's decays at 50% and 75% of W; config 3 uses the same
+    # step-decay shape, reading C27)
+    "2": dict(W=64000 * 128, B=128, s=(1, 16), Wb=[32000 * 128, 48000 * 128], factors=[0.1, 0.01]),
+    "3": dict(W=64000 * 128, B=128, s=(1, 8), Wb=[32000 * 128, 48000 * 128], factors=[0.1, 0.01]),
+}
+
+
+def asp_workload_events(n: int, n_push: int, ver0: int, jitter: int = 100, seed: int = 7, period: int = 1000):
+    """Arrival order of an ASP phase from the seeded integer-tick schedule (ss_schedule, DESIGN reading C7: every
+    worker pulls at t = 0, then each push is followed by the pusher's pull) with the version each worker sends: the
+    version of its last pull. Returns (kind, worker, version) int arrays; the phase starts at ver0."""
+    import numpy as np
+    from paper_2104_08364_b200 import syncswitch as ss
+    s, (kind, worker, _) = ss.ss_schedule(n, [period] * n, n_push, jitter=jitter, seed=seed)
+    ss.ss_check(s)
+    version = np.zeros(kind.size, dtype=np.int64)
+    base = [ver0] * n
+    ver = ver0
+    for e in range(kind.size):
+        j = int(worker[e])
+        if kind[e] == 1:
+            base[j] = ver
+            version[e] = ver
+        else:
+            version[e] = base[j]
+            ver += 1
+    return kind, worker, version
+
+
+def run_workload(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2104_08364_b200 import syncswitch as ss
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, wl = CONFIGS[args.config], WORKLOADS[args.config]
+    P, n, S, win = cfg["P"], cfg["n"], cfg["S"], args.window or cfg["window"]
+    hosted = [j for j in range(n) if (j * world) // n == rank]
+    fused = (1 if n <= world else 2) if args.fused == "auto" else int(args.fused)
+    w0 = torch.empty(P, device="cuda")
+    ss.ss_check(ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0))
+    w0.mul_(64.0)
+    ring = {(j, r): torch.empty(P, device="cuda") for j in hosted for r in range(2)}
+    for (j, r), buf in ring.items():
+        ss.ss_check(ss.ss_synth_grad(SEED, j, r, 0, P, buf))
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_run(s_num, s_den, scale=1):
+        """One whole workload (steps / scale) from a fresh context; returns the run's record."""
+        s, (n_bsp, n_asp, bounds) = ss.ss_table1(wl["W"], wl["B"], n, s_num, s_den, wl["Wb"])
+        ss.ss_check(s)
+        n_bsp, n_asp = n_bsp // scale, n_asp // scale
+        g = ss.SyncSwitch(w0, S, n, 0.1, 0.9)
+        if world > 1:
+            uid = [ss.ss_nccl_unique_id() if rank == 0 else None]      # one NCCL id per communicator
+            dist.broadcast_object_list(uid, src=0)
+            g.init_dist(rank, world, uid[0])
+            g.set_fused(fused)
+        g.set_window(win)
+        g.set_lr_schedule(bounds, wl["factors"])
+        if world > 1 and fused:
+            dst = {j: g.pull_buffer(j) for j in hosted}
+        else:
+            dst = {j: ss.ptr(t) for j, t in pull_bufs.items()}
+        # BSP supersteps: step t feeds ring slot t mod 2 of every hosted worker
+        gp = [(ctypes.c_void_p * max(len(hosted), 1))(*[ss.ptr(ring[(j, r)]) for j in hosted]) for r in range(2)]
+        ws = np.array(hosted, dtype=np.int32)
+        vs = np.zeros(max(len(hosted), 1), dtype=np.int64)
+        kind, worker, version = asp_workload_events(n, n_asp, n_bsp)
+        evs = (ss.ss_event * max(kind.size, 1))()
+        cnt = [0] * n
+        for e in range(kind.size):
+            j = int(worker[e])
+            if kind[e] == 0:
+                buf = ring.get((j, cnt[j] % 2))
+                cnt[j] += 1
+                evs[e] = ss.ss_event(0, j, int(version[e]), ss.ptr(buf) if buf is not None else None, None)
+            else:
+                evs[e] = ss.ss_event(1, j, int(version[e]), None, dst.get(j))
+        stream = torch.cuda.ExternalStream(g.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        L, c = ss.lib, g.ctx
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for t in range(n_bsp):
+            vs[:] = t
+            st = L.ss_bsp_step(c, ctypes.cast(gp[t % 2], ctypes.c_void_p), ws.ctypes.data, vs.ctypes.data,
+                               len(hosted))
+            if st:
+                raise ss.SSError(st, g.last_error())
+        if n_asp:
+            ss.ss_check(L.ss_switch(c, ss.SS_ASP, 0))
+            st = L.ss_asp_replay(c, ctypes.cast(evs, ctypes.c_void_p), kind.size, None)
+            if st:
+                raise ss.SSError(st, g.last_error())
+        g.sync()
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        tt = torch.tensor([e0.elapsed_time(e1) / 1e3, wall], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_s, wall_s = tt.tolist()
+        stt = g.stats(256)
+        assert stt["status"] == 0 and stt["version"] == n_bsp + n_asp, (stt, g.last_error())
+        hist = [int(x) for x in stt["hist"]]
+        top = max((i for i, x in enumerate(hist) if x), default=0)
+        g.close()
+        return {"s": f"{s_num}/{s_den}", "bsp_steps": n_bsp, "asp_pushes": n_asp, "lr_boundaries_version": bounds,
+                "seconds": dev_s, "wall_seconds": wall_s, "samples_per_s": wl["W"] / scale / dev_s,
+                "staleness_hist": {str(i): hist[i] for i in range(top + 1) if hist[i]},
+                "max_staleness": top}
+
+    pull_bufs = {} if (world > 1 and fused) else {j: torch.empty(P, device="cuda") for j in hosted}
+    one_run(1, 2, scale=100)                         # warm-up: kernels loaded, peer mappings exercised
+    clocks = Clocks(local)
+    clocks.start()
+    runs = {"bsp": one_run(1, 1), "asp": one_run(0, 1), "switched": one_run(*wl["s"])}
+    clk = clocks.stop()
+    sw = runs["switched"]
+    line = {"metric": METRIC, "value": round(sw["seconds"], 4),
+            "unit": "s of sync-only time for the whole workload (switched protocol)", "n_gpus": world,
+            "steps": sw["bsp_steps"] + sw["asp_pushes"], "warmup": 1, "ms_per_step": None,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded counter-hash gradients, 2-slot rings per worker)",
+            "config": {"workload": cfg["name"] + f"; whole workload W={wl['W']} samples, B={wl['B']}, switched at "
+                                                 f"s={wl['s'][0]}/{wl['s'][1]} (Table I remap)",
+                       "P": P, "n_workers": n, "n_shards": S, "asp_window_events": win,
+                       "exchange": "single GPU" if world == 1 else
+                       ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed"][fused],
+                       "schedule": "ss_schedule, period 1000 ticks, jitter 100, seed 7; each push followed by its pull"},
+            "runs": runs,
+            "speedup_vs_bsp": {k: runs["bsp"]["seconds"] / r["seconds"] for k, r in runs.items()},
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def _oracle_step(orc, o, n, grads_bsp, grads_asp):
     ver = o.version
     assert o.bsp_step(grads_bsp, versions=[ver] * n) == 0
@@ -498,5 +664,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.config == "4":
         run_scenario(a)
+    elif a.workload:
+        run_workload(a)
     else:
         run_ours(a)
