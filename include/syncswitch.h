@@ -91,6 +91,11 @@ ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *ncc
  * SS_NVLS=0/1 overrides. Errors: SS_E_INVAL. */
 ss_status ss_set_fused(ss_ctx *ctx, int32_t mode);
 
+/* The exchange in effect: *mode = the ss_set_fused mode (0 on a single GPU), *nvls = 1 once the fused path has set up
+ * its NVSwitch multicast replica (decided collectively at the first fused call), else 0. Any output may be NULL.
+ * Errors: none besides a diverged context. */
+ss_status ss_get_exchange(ss_ctx *ctx, int32_t *mode, int32_t *nvls);
+
 /* Fused multi-GPU mode: the CUDA-IPC-mapped pull buffer (device fp32[P_pad], owned by the context, valid until
  * ss_destroy) of a worker hosted on this rank. Owners store each pull's snapshot slices into it over NVLink; passing
  * it as ss_pull's dst makes the pull zero-copy (otherwise the snapshot is copied from it into dst). Collective on

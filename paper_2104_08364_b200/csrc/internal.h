@@ -21,6 +21,7 @@ struct PeerSync {
   uint32_t wait_epoch;              // !=0: every CTA waits for flag >= wait_epoch from all ranks before starting
   uint32_t signal_epoch;            // !=0: the last CTA to finish signals every rank with signal_epoch
   int32_t end_wait;                 // and then waits until every rank has signalled signal_epoch
+  unsigned long long *trace;        // SS_TRACE: CTA 0 / the last CTA record globaltimer into trace[0..3] (or null)
 };
 
 // bsp_update (SV §2.5 K1): out-of-place aggregate of n_in inputs in ascending order, mean by `divisor`,

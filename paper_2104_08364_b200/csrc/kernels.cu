@@ -14,6 +14,7 @@
 // v = fma(mu, v, g), w = fma(-eta, v, w).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -50,6 +51,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Block-wide: returns when every rank has signalled >= epoch (or on timeout).
+// SS_TRACE timestamps (globaltimer ns) of one fused launch: [0] CTA 0 entered, [1] CTA 0's start wait satisfied,
+// [2] the last CTA about to signal, [3] the last CTA's end wait satisfied.
+__device__ __forceinline__ void trace_mark(const PeerSync &s, int k) {
+  if (s.trace != nullptr && threadIdx.x == 0) s.trace[k] = globaltimer();
+}
+
 __device__ void peer_wait(const PeerSync &s, uint32_t epoch) {
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer();
@@ -68,6 +75,15 @@ __device__ void peer_wait(const PeerSync &s, uint32_t epoch) {
   __syncthreads();
 }
 
+// Block-wide, at kernel entry: CTA 0 stamps trace[0]; every CTA waits for wait_epoch when set (CTA 0 stamps trace[1]).
+__device__ __forceinline__ void peer_enter(const PeerSync &s) {
+  if (blockIdx.x == 0) trace_mark(s, 0);
+  if (s.wait_epoch) {
+    peer_wait(s, s.wait_epoch);
+    if (blockIdx.x == 0) trace_mark(s, 1);
+  }
+}
+
 // Block-wide, at kernel end: the last CTA of the grid publishes signal_epoch to every rank (after a system-scope fence
 // that orders all of this grid's stores, local and remote, before the flag) and optionally waits for all ranks.
 __device__ void peer_done(const PeerSync &s) {
@@ -81,9 +97,13 @@ __device__ void peer_done(const PeerSync &s) {
   if (threadIdx.x == 0) {
     *s.ctr = 0;
     __threadfence_system();
+    trace_mark(s, 2);
     for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, s.signal_epoch);
   }
-  if (s.end_wait) peer_wait(s, s.signal_epoch);
+  if (s.end_wait) {
+    peer_wait(s, s.signal_epoch);
+    trace_mark(s, 3);
+  }
 }
 
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
@@ -127,7 +147,7 @@ constexpr int kG1 = 8;  // gradients loaded together
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
-  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
+  peer_enter(a.sync);
   const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -272,7 +292,7 @@ constexpr int kU2 = 4;
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_constant__ AspArgs a) {
-  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
+  peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const float lam = a.lam;
@@ -405,7 +425,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
-  if (a.sync.wait_epoch) peer_wait(a.sync, a.sync.wait_epoch);
+  peer_enter(a.sync);
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int push_ev[kMaxEvents];
@@ -521,6 +541,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
 // scatter (fused path): every hosted gradient's owner slices go to the owners' inboxes with
 // posted 128-bit NVLink stores (the local slice is read in place by the owner update, never copied).
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
+  peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int me = a.sync.rank, G = a.sync.world;
@@ -552,50 +573,52 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 
 // scatter_sum (fused mode 2): one pass over the hosted gradients — sum them in ascending order and store each owner's
 // slice of the pre-sum straight into that owner's inbox slot a.slot[0] (this rank's id); the own slice stays local.
+// The grid is split into G interleaved CTA subsets, subset k serving destination region (me + 1 + k) % G: the NVLink
+// stores to every peer and the local-only pass over the own region run at the same time (processing the regions one
+// after another left the own region's HBM pass on the critical path after the NVLink-bound ones).
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
+  const int k = (int)(blockIdx.x % G);
+  const int64_t n_cta = ((int64_t)gridDim.x - k + G - 1) / G;             // CTAs in subset k
+  const int64_t tid = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
+  const int64_t stride = n_cta * blockDim.x;
   const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
   constexpr int U = 2;
-  // destination regions in rotated order (me+1, ..., me): the ranks write to distinct receivers at any moment, and
-  // the own region (a local store) comes last
-  for (int step = 1; step <= G; ++step) {
-    const int r = (me + step) % G;
-    const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
-    float *dst = a.inbox[r] + slot_off;
-    const int64_t n4 = cnt >> 2;
-    for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
-      float4 acc[U];
+  const int r = (me + 1 + k) % G;
+  const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
+  float *dst = a.inbox[r] + slot_off;
+  const int64_t n4 = cnt >> 2;
+  for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+    float4 acc[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t q = q0 + u * stride;
-        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (q < n4 && a.n_src > 0) acc[u] = ld4(a.src[0] + lo + 4 * q);
-      }
-      for (int j0 = 1; j0 < a.n_src; j0 += kG1) {
-        float4 t[kG1][U];
-#pragma unroll
-        for (int jj = 0; jj < kG1; ++jj)
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (j0 + jj < a.n_src && q0 + u * stride < n4) t[jj][u] = ld4(a.src[j0 + jj] + lo + 4 * (q0 + u * stride));
-#pragma unroll
-        for (int jj = 0; jj < kG1; ++jj)
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (j0 + jj < a.n_src && q0 + u * stride < n4) acc[u] = add4(acc[u], t[jj][u]);  // ascending
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = acc[u];
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < n4 && a.n_src > 0) acc[u] = ld4(a.src[0] + lo + 4 * q);
     }
-    const int64_t i = 4 * n4 + tid;  // scalar tail of the segment
-    if (i < cnt) {
-      float acc = a.n_src > 0 ? a.src[0][lo + i] : 0.0f;
-      for (int k = 1; k < a.n_src; ++k) acc = __fadd_rn(acc, a.src[k][lo + i]);
-      dst[i] = acc;
+    for (int j0 = 1; j0 < a.n_src; j0 += kG1) {
+      float4 t[kG1][U];
+#pragma unroll
+      for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + jj < a.n_src && q0 + u * stride < n4) t[jj][u] = ld4(a.src[j0 + jj] + lo + 4 * (q0 + u * stride));
+#pragma unroll
+      for (int jj = 0; jj < kG1; ++jj)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j0 + jj < a.n_src && q0 + u * stride < n4) acc[u] = add4(acc[u], t[jj][u]);  // ascending
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = acc[u];
+  }
+  const int64_t i = 4 * n4 + tid;  // scalar tail of the region
+  if (i < cnt) {
+    float acc = a.n_src > 0 ? a.src[0][lo + i] : 0.0f;
+    for (int j = 1; j < a.n_src; ++j) acc = __fadd_rn(acc, a.src[j][lo + i]);
+    dst[i] = acc;
   }
   peer_done(a.sync);
 }
@@ -1011,7 +1034,9 @@ cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s) {
 
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
-  k<<<grid_for(k, (a.P / 4 + 1) / 2 + 1), kThreads, 0, s>>>(a);
+  const int G = a.sync.world > 0 ? a.sync.world : 1;
+  const int grid = (std::max(grid_for(k, (a.P / 4 + 1) / 2 + 1), G) + G - 1) / G * G;   // every subset has CTAs
+  k<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,10 @@ struct ss_ctx {
   uint64_t cap_ddropped = 0;
   std::vector<int64_t> cap_base0, cap_log;   // log records appended during the captured step
   // instrumentation
+  unsigned long long *trace_dev = nullptr;   // SS_TRACE=<prefix>: 4 globaltimer stamps per fused launch
+  int64_t trace_cap = 0;
+  std::vector<int8_t> trace_kind;            // per recorded launch: 0 scatter, 1 scatter_sum, 2 bsp_update, 3 asp_replay
+  std::string trace_path;
   bool prof = false;
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> event_pool;
@@ -425,6 +429,13 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   slots = std::max<int64_t>(slots, std::max<int64_t>(c->n, c->max_win));
   SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
   if (!c->pbuf) SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+  if (!c->trace_dev && getenv("SS_TRACE") && getenv("SS_TRACE")[0]) {
+    c->trace_path = getenv("SS_TRACE");
+    const char *cap = getenv("SS_TRACE_CAP");
+    c->trace_cap = cap ? std::max<int64_t>(1, atoll(cap)) : 65536;
+    SS_CUDA(c, cudaMalloc(&c->trace_dev, (size_t)c->trace_cap * 4 * sizeof(unsigned long long)));
+    SS_CUDA(c, cudaMemset(c->trace_dev, 0, (size_t)c->trace_cap * 4 * sizeof(unsigned long long)));
+  }
   if (!c->sigblk) {
     SS_CUDA(c, cudaMalloc(&c->sigblk, ss::kSigWords * sizeof(uint32_t)));
     SS_CUDA(c, cudaMemset(c->sigblk, 0, ss::kSigWords * sizeof(uint32_t)));
@@ -471,9 +482,13 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   return SS_OK;
 }
 
-ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bool end_wait) {
+ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bool end_wait, int kind) {
   ss::PeerSync p;
   std::memset(&p, 0, sizeof p);
+  if (c->trace_dev && (int64_t)c->trace_kind.size() < c->trace_cap) {
+    p.trace = c->trace_dev + 4 * c->trace_kind.size();
+    c->trace_kind.push_back((int8_t)kind);
+  }
   p.sig_local = c->sigblk;
   for (int32_t q = 0; q < c->world; ++q) p.sig_peer[q] = c->peer_sig[q];
   p.ctr = c->sigblk + 32;
@@ -499,7 +514,7 @@ ss_status launch_scatter(ss_ctx *c, const std::vector<std::pair<const float *, i
   for (int32_t q = 0; q < c->world; ++q) a.inbox[q] = c->peer_inbox[q];
   a.reg_len = c->reg_len;
   a.P = c->P;
-  a.sync = peer_sync(c, 0, epoch, false);
+  a.sync = peer_sync(c, 0, epoch, false, 0);
   Timed t;
   double remote = 0.0;  // elements of the other ranks' regions
   for (int32_t q = 0; q < c->world; ++q)
@@ -562,7 +577,7 @@ ss_status flush_fused(ss_ctx *c) {
   a.flag = c->flag;
   a.count = cnt;
   a.lam = c->lam;
-  a.sync = peer_sync(c, epA, epB, true);
+  a.sync = peer_sync(c, epA, epB, true, 3);
   Timed t;
   timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
   SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
@@ -838,6 +853,23 @@ void ss_destroy(ss_ctx *c) {
     flush(c);
     cudaStreamSynchronize(c->stream);
   }
+  if (c->trace_dev) {   // SS_TRACE dump: <prefix>.rank<r>.csv, one row per fused launch
+    std::vector<unsigned long long> h(4 * c->trace_kind.size());
+    if (!h.empty() &&
+        cudaMemcpy(h.data(), c->trace_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+            cudaSuccess) {
+      const std::string path = c->trace_path + ".rank" + std::to_string(c->rank) + ".csv";
+      if (FILE *f = fopen(path.c_str(), "w")) {
+        static const char *names[] = {"scatter", "scatter_sum", "bsp_update", "asp_replay", "pipe_bsp"};
+        fprintf(f, "launch,kernel,enter_ns,waited_ns,signal_ns,end_ns\n");
+        for (size_t i = 0; i < c->trace_kind.size(); ++i)
+          fprintf(f, "%zu,%s,%llu,%llu,%llu,%llu\n", i, names[c->trace_kind[i]], h[4 * i], h[4 * i + 1],
+                  h[4 * i + 2], h[4 * i + 3]);
+        fclose(f);
+      }
+    }
+    cudaFree(c->trace_dev);
+  }
   for (auto &t : c->timed) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -1033,7 +1065,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     pa.lam = a.lam;
     pa.work = c->sigblk + 96;
     pa.epoch = epA;
-    pa.sync = peer_sync(c, 0, epB, true);
+    pa.sync = peer_sync(c, 0, epB, true, 4);
     Timed t;
     const double cnt_me = (double)(c->real_hi[me] - lo);
     timed_begin(c, &t, 0, 4.0 * cnt_me * (ni + 4));
@@ -1063,7 +1095,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       for (int32_t q = 0; q < c->world; ++q) sa.inbox[q] = c->peer_inbox[q];
       sa.reg_len = c->reg_len;
       sa.P = c->P;
-      sa.sync = peer_sync(c, 0, epA, false);
+      sa.sync = peer_sync(c, 0, epA, false, 1);
       Timed t;
       double remote = 0.0;
       for (int32_t q = 0; q < c->world; ++q)
@@ -1099,7 +1131,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       for (int32_t step = 1; step < c->world; ++step)   // rotated: the ranks' stores go to distinct receivers
         a.bcast[a.n_bcast++] = c->peer_w[(me + step) % c->world] + lo;
     }
-    a.sync = peer_sync(c, epA, epB, true);
+    a.sync = peer_sync(c, epA, epB, true, 2);
     Timed t;
     timed_begin(c, &t, 0, 4.0 * (double)cnt * (a.n_in + 4), 4.0 * (double)cnt * (c->nvls.ready ? 1 : a.n_bcast));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
@@ -1372,6 +1404,13 @@ ss_status ss_set_fused(ss_ctx *c, int32_t mode) {
   if (mode < 0 || mode > 2) return fail(c, SS_E_INVAL, "fused mode must be 0, 1 or 2");
   SS_TRY(flush(c));
   c->fused_mode = mode;
+  return SS_OK;
+}
+
+ss_status ss_get_exchange(ss_ctx *c, int32_t *mode, int32_t *nvls) {
+  SS_TRY(check_live(c));
+  if (mode) *mode = c->world > 1 ? c->fused_mode : 0;
+  if (nvls) *nvls = c->nvls.ready ? 1 : 0;
   return SS_OK;
 }
 

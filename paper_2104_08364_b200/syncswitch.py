@@ -30,7 +30,7 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
-           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_pull_buffer",
+           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_get_exchange", "ss_pull_buffer",
            "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked",
            "ss_dynamic_criterion", "ss_criterion_observe", "ss_capture_begin", "ss_capture_end",
            "ss_capture_replay"]
@@ -84,6 +84,7 @@ def _load():
         "ss_init": [p, p, i64, i32, i32, f32, f32],
         "ss_init_dist": [p, i32, i32, p],
         "ss_set_fused": [p, i32],
+        "ss_get_exchange": [p, p, p],
         "ss_pull_buffer": [p, i32, p],
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
@@ -440,6 +441,11 @@ class SyncSwitch:
 
     def set_fused(self, mode: int):
         return self._chk(lib.ss_set_fused(self.ctx, mode))
+
+    def exchange(self) -> dict:
+        m, v = ctypes.c_int32(), ctypes.c_int32()
+        self._chk(lib.ss_get_exchange(self.ctx, ctypes.byref(m), ctypes.byref(v)))
+        return {"fused": m.value, "nvls": bool(v.value)}
 
     def pull_buffer(self, worker: int) -> int:
         out = ctypes.c_void_p()

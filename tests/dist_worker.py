@@ -135,7 +135,7 @@ def main():
         snap_arr = np.stack([s.cpu().numpy().copy() for s in snaps]) if snaps else np.zeros((0, P), np.float32)
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=w, v=v, stale=np.array(stale), log=g.log(),
              hist=st["hist"], version=st["version"], dropped=st["dropped"], snaps=snap_arr,
-             hosted=np.array(hosted))
+             hosted=np.array(hosted), nvls=int(g.exchange()["nvls"]))
     g.close()
     dist.barrier()
     dist.destroy_process_group()

@@ -65,11 +65,11 @@ def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0, idx=None):
     return o, stale, snaps, kind, worker
 
 
-def launch(world, args, tmp):
+def launch(world, args, tmp, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}",
            os.path.join(ROOT, "tests", "dist_worker.py"), "--out", tmp, *map(str, args)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
@@ -171,6 +171,38 @@ def test_multi_gpu_edge_layouts(orc, world, shape, fused):
                        "--bsp2", 2, "--fused", fused], tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 2, 24, 2)
+    cmp = np.array_equal if fused == 1 else close_c13
+    for r in res:
+        assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
+        assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
+        hosted = [int(j) for j in r["hosted"]]
+        exp, cnt = [], {j: 0 for j in hosted}
+        for kd, j in zip(kind, worker):
+            if kd == 1 and int(j) in hosted:
+                exp.append(snaps[int(j)][cnt[int(j)]])
+                cnt[int(j)] += 1
+        assert len(exp) == len(r["snaps"])
+        for a, b in zip(r["snaps"], exp):
+            assert cmp(a, b)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [1, 2])
+@pytest.mark.parametrize("P", [100003, 33])
+def test_multi_gpu_nvls_forced(orc, world, fused, P):
+    """The NVSwitch-multicast broadcast (default from 8 GPUs) forced on at 2 and 4 GPUs (SS_NVLS=1): BSP supersteps
+    store each updated slice once through the multicast view. Same results as the P2P broadcast: bit-exact in
+    fused-exact mode, C13 in pre-summed mode. Skipped when the driver / fabric offers no multicast."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    n, S = 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 7, "--bsp1", 3, "--pushes", 40,
+                       "--bsp2", 3, "--fused", fused], tmp, env={"SS_NVLS": "1"})
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    if not all(int(r["nvls"]) for r in res):
+        pytest.skip("NVLS multicast unavailable on this box")
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 3, 40, 3)
     cmp = np.array_equal if fused == 1 else close_c13
     for r in res:
         assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
