@@ -39,20 +39,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not (force or _stale()):
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Builds the library (out/defines: tuning variants for tools/replay_sweep.py; the product is the default)."""
+    if out is None and not (force or _stale()):
         return LIB
     inc, lib = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
+    target = out or LIB
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
+           *[f"-D{d}" for d in defines],
            *[os.path.join(CSRC, s) for s in SOURCES],
            f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}",
            "-o", tmp]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

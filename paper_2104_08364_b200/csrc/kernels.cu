@@ -394,9 +394,17 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
 // bulk copies (cp.async.bulk, completion on an mbarrier). One CTA walks its tiles (kTmaTile floats = 8 KB); the w and
 // v of a tile live in registers for the whole window; thread 0 keeps kTmaStages tile loads in flight ahead of the
 // consumers, across push and tile boundaries, so the bytes in flight no longer depend on registers per thread.
-constexpr int kTmaTile = 2048;                       // floats per tile: 256 threads x 2 float4
-constexpr int kTmaStages = 6;
-constexpr int kTmaSmem = kTmaStages * kTmaTile * 4;  // 48 KB of dynamic shared memory
+#ifndef SS_TMA_TILE
+#define SS_TMA_TILE 2048   // tuning knobs (tools/replay_sweep.py builds variants)
+#endif
+#ifndef SS_TMA_STAGES
+#define SS_TMA_STAGES 10   // 80 KB rings -> 2 CTAs per SM: 96.5-98% of the HBM copy vs 93% at 6 stages / 4 CTAs
+#endif                     // (profiles/r01_replay_sweep.txt)
+constexpr int kTmaTile = SS_TMA_TILE;                // floats per tile: 256 threads x 2 float4
+constexpr int kTmaStages = SS_TMA_STAGES;
+constexpr int kTmaSmem = kTmaStages * kTmaTile * 4;  // 80 KB of dynamic shared memory
+constexpr int kTU = kTmaTile / (4 * kThreads);       // float4 per thread per tile
+static_assert(kTU >= 1 && kTmaTile % (4 * kThreads) == 0, "tile must be a multiple of 4 x kThreads floats");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -462,10 +470,10 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   for (int64_t tl = 0; tl < my_tiles; ++tl) {
     const int64_t off = (blockIdx.x + tl * gridDim.x) * kTmaTile;
     const int64_t len = min((int64_t)kTmaTile, nvec - off);
-    float4 wv[2], vv[2];
-    bool ok[2];
+    float4 wv[kTU], vv[kTU];
+    bool ok[kTU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kTU; ++u) {
       const int64_t i = 4 * (threadIdx.x + u * kThreads);    // element within the tile
       ok[u] = i < len;
       if (ok[u]) {
@@ -479,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
         mbar_wait(&full[s], (uint32_t)((it / kTmaStages) & 1));
         const float neg_eta = -a.ev[e].lr, mu = a.ev[e].mu;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kTU; ++u) {
           if (!ok[u]) continue;
           float4 g = *reinterpret_cast<const float4 *>(ring + s * kTmaTile + 4 * (threadIdx.x + u * kThreads));
           float *gp = &g.x, *wp = &wv[u].x, *vp = &vv[u].x;
@@ -499,12 +507,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
         ++it;
       } else if (a.ev[e].dst != nullptr) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < kTU; ++u)
           if (ok[u]) st4(a.ev[e].dst + off + 4 * (threadIdx.x + u * kThreads), wv[u]);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kTU; ++u) {
       if (!ok[u]) continue;
       bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
              nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);

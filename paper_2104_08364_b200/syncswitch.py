@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsyncswitch.so")
+LIB_PATH = os.environ.get("SS_LIB_VARIANT") or os.path.join(_PKG, "libsyncswitch.so")   # variant: tuning sweeps
 
 SS_BSP, SS_ASP = 0, 1
 STATUS = ["SS_OK", "SS_E_INVAL", "SS_E_STATE", "SS_E_PROTOCOL", "SS_E_BARRIER", "SS_E_CAUSALITY", "SS_E_DIVERGED",
