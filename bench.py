@@ -332,6 +332,9 @@ def run_ours(args):
                     "bytes_per_launch": d["nvlink_bytes"] / d["launches"], "avg_launch_us": 1e6 * per_launch_s,
                     "peak_source": "measured NVLink peer copy 770 GB/s per direction (B200_PROFILING.md)",
                     "frac_of_nominal_900GBps": round(achieved / 900.0, 4),
+                    # every GPU sending to every peer at once: SM-driven stores reach ~690 GB/s per GPU
+                    # (tools/p2p_bench.cu, profiles/r01_p2p_alltoall_microbench.txt)
+                    "frac_of_alltoall_sm_ceiling_690GBps": round(achieved / 690.0, 4),
                     "hbm_GBps": round(d["bytes"] / d["launches"] / per_launch_s / 1e9, 1), "measured_in": PROF_NOTE}
     else:
         achieved = d["bytes"] / d["launches"] / per_launch_s / 1e9
