@@ -133,6 +133,13 @@ ss_status ss_set_lr_policy(ss_ctx *ctx, int32_t asp_rule, float weight_decay);
  * rounded to fp32 once; BSP supersteps always use the BSP momentum. Errors: SS_E_INVAL. */
 ss_status ss_set_momentum_policy(ss_ctx *ctx, int32_t rule, int64_t samples_per_epoch, int64_t batch);
 
+/* Nesterov momentum (SV §8(f) NEXT-4; the paper never names the momentum form, reading C1 takes the accumulator form
+ * of the prototype's TF MomentumOptimizer; this switch is that optimizer's use_nesterov variant, DESIGN
+ * reading C28): on = 1 -> v = mu*v + g, w = w - eta*(g + mu*v) with each product-sum one fused multiply-add
+ * (fma(mu, v, g) then fma(-eta, ., w)); on = 0 (default) -> w = w - eta*v. Applies to BSP supersteps and ASP pushes
+ * applied after the call (a pending ASP window is flushed first). Errors: SS_E_INVAL (on not 0/1). */
+ss_status ss_set_nesterov(ss_ctx *ctx, int32_t on);
+
 /* BSP barrier set for the elastic straggler policy (SV §8(f) NEXT-2; "removes any detected stragglers from the
  * current cluster so as to complete the specified amount of BSP training free of stragglers. Once the designated BSP
  * workload is fulfilled, it will then restore the cluster size"). workers: `count` distinct ids in [0, n). Later

@@ -73,6 +73,8 @@ def lib():
         g("set_members").argtypes = [_p, _p, _i32]
         g("set_momentum_policy").restype = _i32
         g("set_momentum_policy").argtypes = [_p, _i32, _i64, _i64]
+        g("set_nesterov").restype = _i32
+        g("set_nesterov").argtypes = [_p, _i32]
         g("bsp_step").restype = _i32
         g("bsp_step").argtypes = [_p, _p, _p, _p, _i32]
         g("asp_push").restype = _i32
@@ -196,6 +198,9 @@ class Oracle:
     def set_members(self, workers) -> int:
         w = np.ascontiguousarray(workers, dtype=np.int32)
         return int(self._fn("set_members")(self._h, _ptr(w), w.size))
+
+    def set_nesterov(self, on: bool) -> int:
+        return int(self._fn("set_nesterov")(self._h, int(on)))
 
     def set_momentum_policy(self, rule: int, samples_per_epoch: int = 1, batch: int = 1) -> int:
         return int(self._fn("set_momentum_policy")(self._h, rule, samples_per_epoch, batch))

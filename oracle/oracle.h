@@ -56,6 +56,7 @@ typedef struct orc_d orc_d;
   int32_t orc##SUF##_set_lr_schedule(orc_##SUF *o, const int64_t *bounds, const float *factors, int32_t nb);     \
   int32_t orc##SUF##_set_lr_policy(orc_##SUF *o, int32_t asp_rule, float weight_decay);                          \
   int32_t orc##SUF##_set_momentum_policy(orc_##SUF *o, int32_t rule, int64_t samples_per_epoch, int64_t batch);   \
+  int32_t orc##SUF##_set_nesterov(orc_##SUF *o, int32_t on);                                                    \
   int32_t orc##SUF##_set_members(orc_##SUF *o, const int32_t *workers, int32_t count);                           \
   int32_t orc##SUF##_bsp_step(orc_##SUF *o, const REAL *const *grads, const int32_t *workers,                     \
                               const int64_t *versions, int32_t n_local);                                         \

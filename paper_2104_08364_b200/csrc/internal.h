@@ -38,6 +38,7 @@ struct BspArgs {
   float mu;
   float neg_eta;
   float lam;
+  int32_t nesterov;         // 1: w -= eta * (g + mu * v_new) (ss_set_nesterov), else w -= eta * v_new
   float *bcast[kMaxPeers];  // fused path: remote replicas (at this slice's offset) that receive the updated w
   int32_t n_bcast;
   float *mc_w;              // NVLS: multicast view of this slice; one multimem.st updates every replica
@@ -70,6 +71,7 @@ struct AspArgs {
   int64_t count;
   int32_t n_ev;
   float lam;
+  int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;
 };
 
@@ -115,6 +117,7 @@ struct PipeBspArgs {
   int32_t n_bcast;
   int *flag;
   float divisor, mu, neg_eta, lam;
+  int32_t nesterov;
   uint32_t *work;                // item counter (local; the last CTA resets it)
   uint32_t epoch;                // chunk-flag epoch of this step
   PeerSync sync;                 // end barrier: signal + wait

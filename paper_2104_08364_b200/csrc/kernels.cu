@@ -127,11 +127,12 @@ __device__ __forceinline__ void mc_st1(float *p, float x) {
 struct Upd {
   float divisor, recip, mu, neg_eta, lam;
   bool use_recip;
+  bool nesterov;
   __device__ __forceinline__ void operator()(float a, float &w, float &v) const {
     float g = use_recip ? __fmul_rn(a, recip) : __fdiv_rn(a, divisor);
     if (lam != 0.0f) g = __fmaf_rn(lam, w, g);
     v = __fmaf_rn(mu, v, g);
-    w = __fmaf_rn(neg_eta, v, w);
+    w = __fmaf_rn(neg_eta, nesterov ? __fmaf_rn(mu, v, g) : v, w);   // Nesterov: step along g + mu*v_new
   }
 };
 
@@ -148,7 +149,7 @@ constexpr int kG1 = 8;  // gradients loaded together
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
   peer_enter(a.sync);
-  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
+  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
@@ -301,10 +302,11 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
   while (first_push < a.n_ev && a.ev[first_push].kind != 0) ++first_push;
 
   // per-push momentum: the post-switch momentum policy may vary it push by push
+  const bool nest = a.nesterov != 0;
   auto apply1 = [&](float g, float &w, float &v, float neg_eta, float mu) {
     if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
     v = __fmaf_rn(mu, v, g);
-    w = __fmaf_rn(neg_eta, v, w);
+    w = __fmaf_rn(neg_eta, nest ? __fmaf_rn(mu, v, g) : v, w);
   };
 
   if (VEC) {
@@ -496,7 +498,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
             float gg = gp[c];
             if (lam != 0.0f) gg = __fmaf_rn(lam, wp[c], gg);   // g + f(w) at the PS's current w
             vp[c] = __fmaf_rn(mu, vp[c], gg);
-            wp[c] = __fmaf_rn(neg_eta, vp[c], wp[c]);
+            wp[c] = __fmaf_rn(neg_eta, a.nesterov ? __fmaf_rn(mu, vp[c], gg) : vp[c], wp[c]);
           }
         }
         __syncthreads();                                        // every thread is done with stage s
@@ -531,7 +533,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
           float gg = a.ev[e].src[i];
           if (lam != 0.0f) gg = __fmaf_rn(lam, w, gg);
           v = __fmaf_rn(a.ev[e].mu, v, gg);
-          w = __fmaf_rn(-a.ev[e].lr, v, w);
+          w = __fmaf_rn(-a.ev[e].lr, a.nesterov ? __fmaf_rn(a.ev[e].mu, v, gg) : v, w);
         } else if (a.ev[e].dst) {
           a.ev[e].dst[i] = w;
         }
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constan
   const uint32_t nA = (uint32_t)(G * a.max_chunks);
   const uint32_t nB = (uint32_t)a.n_chunks[me];
   const bool roleA = blockIdx.x < (gridDim.x + 1) / 2;
-  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor)};
+  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
   bool bad = false;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(a.work + (roleA ? 0 : 1), 1u);

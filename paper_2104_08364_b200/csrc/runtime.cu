@@ -61,6 +61,7 @@ struct ss_ctx {
   int32_t S = 0, n = 0;
   std::vector<int64_t> off;
   float eta = 0.f, mu = 0.f, lam = 0.f;
+  int32_t nesterov = 0;                // ss_set_nesterov
   int32_t asp_rule = 0;
   int32_t mom_rule = 0;                // post-switch momentum policy: 0 same mu, 1 zero, 2 1/n, 3 2^i/n, 4 i/n
   int64_t mom_epoch_samples = 1, mom_batch = 1;
@@ -577,6 +578,7 @@ ss_status flush_fused(ss_ctx *c) {
   a.flag = c->flag;
   a.count = cnt;
   a.lam = c->lam;
+  a.nesterov = c->nesterov;
   a.sync = peer_sync(c, epA, epB, true, 3);
   Timed t;
   timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
@@ -666,6 +668,8 @@ ss_status flush(ss_ctx *c) {
       a.flag = c->flag;
       a.count = cnt;
       a.lam = c->lam;
+      a.nesterov = c->nesterov;
+  a.nesterov = c->nesterov;
       Timed t;
       timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
       SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
@@ -921,6 +925,14 @@ ss_status ss_set_lr_policy(ss_ctx *c, int32_t asp_rule, float weight_decay) {
   return SS_OK;
 }
 
+ss_status ss_set_nesterov(ss_ctx *c, int32_t on) {
+  SS_TRY(check_live(c));
+  if (on != 0 && on != 1) return fail(c, SS_E_INVAL, "nesterov must be 0 or 1");
+  SS_TRY(flush(c));  // queued pushes are applied under the setting they were issued under
+  c->nesterov = on;
+  return SS_OK;
+}
+
 ss_status ss_set_momentum_policy(ss_ctx *c, int32_t rule, int64_t samples_per_epoch, int64_t batch) {
   SS_TRY(check_live(c));
   if (rule < 0 || rule > 4 || samples_per_epoch < 1 || batch < 1) return fail(c, SS_E_INVAL, "bad momentum policy");
@@ -1005,6 +1017,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   a.mu = c->mu;
   a.neg_eta = -eta_t;
   a.lam = c->lam;
+  a.nesterov = c->nesterov;
   if (c->world == 1) {
     a.n_in = k;
     a.w = c->w;
@@ -1063,6 +1076,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     pa.mu = a.mu;
     pa.neg_eta = a.neg_eta;
     pa.lam = a.lam;
+    pa.nesterov = a.nesterov;
     pa.work = c->sigblk + 96;
     pa.epoch = epA;
     pa.sync = peer_sync(c, 0, epB, true, 4);

@@ -30,7 +30,7 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
-           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_get_exchange", "ss_pull_buffer",
+           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_set_nesterov", "ss_get_exchange", "ss_pull_buffer",
            "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked",
            "ss_dynamic_criterion", "ss_criterion_observe", "ss_capture_begin", "ss_capture_end",
            "ss_capture_replay"]
@@ -85,6 +85,7 @@ def _load():
         "ss_init_dist": [p, i32, i32, p],
         "ss_set_fused": [p, i32],
         "ss_get_exchange": [p, p, p],
+        "ss_set_nesterov": [p, i32],
         "ss_pull_buffer": [p, i32, p],
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
@@ -415,13 +416,14 @@ class SyncSwitch:
         if n_params is None:
             n_params = int(params.numel() if hasattr(params, "numel") else np.asarray(params).size)
         self.P, self.n, self.S = n_params, n_workers, n_shards
+        self._destroy = lib.ss_destroy   # held by the instance: still callable during interpreter shutdown
         s, self.ctx = ss_init(params, n_params, n_shards, n_workers, lr, momentum)
         if s != SS_OK:
             raise SSError(s, "ss_init failed")
 
     def close(self):
         if getattr(self, "ctx", None):
-            ss_destroy(self.ctx)
+            self._destroy(self.ctx)
             self.ctx = None
 
     def __del__(self):
@@ -461,6 +463,9 @@ class SyncSwitch:
     def set_members(self, workers):
         w = _a(workers, np.int32)
         return self._chk(lib.ss_set_members(self.ctx, w.ctypes.data, w.size))
+
+    def set_nesterov(self, on: bool):
+        return self._chk(lib.ss_set_nesterov(self.ctx, int(on)))
 
     def set_momentum_policy(self, rule: int, samples_per_epoch: int = 1, batch: int = 1):
         return self._chk(lib.ss_set_momentum_policy(self.ctx, rule, samples_per_epoch, batch))

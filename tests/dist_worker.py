@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--sample", type=int, default=0, help="save only this many sampled elements (full-size runs)")
     ap.add_argument("--host-buffers", type=int, default=0, help="gradients and pull destinations in host memory")
     ap.add_argument("--scenario", type=int, default=-1, help="run ss_scenario_run with this policy instead")
+    ap.add_argument("--nesterov", type=int, default=0)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -59,6 +60,8 @@ def main():
     g.init_dist(rank, world, uid[0])
     if a.fused >= 0:
         g.set_fused(a.fused)
+    if a.nesterov:
+        g.set_nesterov(True)
     g.set_window(a.window)
     g.set_lr_schedule([a.bsp1 + 10], [0.5])
     counter = {j: 0 for j in range(n)}

@@ -426,6 +426,51 @@ def test_config1_toy_end_to_end(ss, orc):
     g.close()
 
 
+@pytest.mark.parametrize("P,off", [(5003, 0), (4099, 1)])
+def test_nesterov_bit_exact(ss, orc, P, off):
+    """Nesterov momentum (reading C28) through bsp_update and the replay kernels (TMA form for 16-byte-aligned
+    buffers, the scalar form for misaligned ones; ragged P), bit-exact with the fp32 oracle."""
+    n, S = 4, 3
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    g.set_nesterov(True)
+    assert o.set_nesterov(True) == 0
+    keep = []
+
+    def dev(j, k):
+        buf = torch.empty(P + off, device="cuda")
+        ss.ss_check(ss.ss_synth_grad(SEED, j, k, 0, P, buf[off:]))
+        keep.append(buf)
+        return buf[off:]
+
+    for step in range(3):
+        g.bsp_step([dev(j, step) for j in range(n)])
+        assert o.bsp_step([host_synth(orc, j, step, P) for j in range(n)]) == 0
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    g.set_window(6)
+    kind, worker, _ = orc.schedule(n, [1000, 1100, 1300, 1600], 24, jitter=100, seed=9)
+    base_g, base_o, cnt = {}, {}, collections.Counter()
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            base_g[j] = g.pull(j)
+            base_o[j] = o.pull(j, False)[2]
+        else:
+            k = 3 + cnt[j]
+            cnt[j] += 1
+            assert g.asp_push(j, dev(j, k), base_g[j]) == o.asp_push(j, host_synth(orc, j, k, P), base_o[j])[1]
+    g.switch(BSP, 0)
+    o.switch(BSP, 0)
+    g.bsp_step([dev(j, 100) for j in range(n)])
+    assert o.bsp_step([host_synth(orc, j, 100, P) for j in range(n)]) == 0
+    g.sync()
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert np.array_equal(g.log(), o.log())
+    g.close()
+
+
 @pytest.mark.parametrize("rule", [1, 2, 3, 4])
 def test_momentum_policies_bit_exact(ss, orc, rule):
     """Post-switch momentum variants: per-push momentum in the replay kernel, bit-exact with the oracle."""

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SEED = 20241018
 
 
-def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0, idx=None):
+def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0, idx=None, nesterov=False):
     """The dist_worker call sequence on the oracle; with `idx`, on those elements only (elementwise update: exact for
     them by shard invariance)."""
     if idx is None:
@@ -30,6 +30,7 @@ def oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop=-1, bsp_drop=0, idx=None):
         S = 1
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
     o.set_lr_schedule([bsp1 + 10], [0.5])
+    o.set_nesterov(nesterov)
     counter = {j: 0 for j in range(n)}
 
     def grad(j):
@@ -81,20 +82,22 @@ def close_c13(x, y, rel=1e-5):
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", ["asp_only", "switched", "switched_fused", "switched_presum", "elastic_fused",
-                                  "elastic_nccl"])
+                                  "elastic_nccl", "nesterov_fused"])
 def test_multi_gpu_parity(orc, world, case):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     P, n, S, win = 100003, 8, 8, 7
     bsp1, pushes, bsp2 = (0, 80, 0) if case == "asp_only" else (3, 60, 2)
-    fused = {"switched_fused": 1, "switched_presum": 2, "elastic_fused": 1}.get(case, 0)
+    fused = {"switched_fused": 1, "switched_presum": 2, "elastic_fused": 1, "nesterov_fused": 1}.get(case, 0)
+    nest = case.startswith("nesterov")
     drop, bsp_drop = (1, 3) if case.startswith("elastic") else (-1, 0)
     with tempfile.TemporaryDirectory() as tmp:
         launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", win, "--bsp1", bsp1, "--pushes", pushes,
-                       "--bsp2", bsp2, "--fused", fused, "--drop", drop, "--bsp-drop", bsp_drop], tmp)
+                       "--bsp2", bsp2, "--fused", fused, "--drop", drop, "--bsp-drop", bsp_drop, "--nesterov", int(nest)],
+               tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
-    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop, bsp_drop)
-    exact = case in ("asp_only", "switched_fused", "elastic_fused")   # NCCL / pre-summed: other sum orders (C13)
+    o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop, bsp_drop, nesterov=nest)
+    exact = case in ("asp_only", "switched_fused", "elastic_fused", "nesterov_fused")   # NCCL / pre-summed: other sum orders (C13)
     ow, ov = o.params(), o.velocity()
     for r in res:
         # protocol integers: exact on every rank

@@ -133,6 +133,55 @@ def test_momentum_quadratic_closed_form(orc):
         assert xs[t - 1] == pytest.approx(want, rel=1e-12, abs=1e-14)
 
 
+def test_nesterov_quadratic_closed_form(orc):
+    # Nesterov (reading C28): v' = mu v + g, x' = x - eta (g + mu v'). On L = a x^2 / 2 (g = a x) the state is linear:
+    # [v', x'] = N [v, x], N = [[mu, a], [-eta mu^2, 1 - eta a (1 + mu)]] (substitute v' into the x update).
+    a, eta, mu, x0 = 0.75, 0.125, float(np.float32(0.9)), 2.0
+    o = orc.Oracle([x0], 1, 1, eta, mu, dtype=np.float64)
+    assert o.set_nesterov(True) == 0
+    xs = []
+    for _ in range(50):
+        x = o.params()[0]
+        assert o.bsp_step([[a * x]]) == 0
+        xs.append(o.params()[0])
+    N = np.array([[mu, a], [-eta * mu * mu, 1 - eta * a * (1 + mu)]])
+    for t in range(1, 51):
+        want = (np.linalg.matrix_power(N, t) @ np.array([0.0, x0]))[1]
+        assert xs[t - 1] == pytest.approx(want, rel=1e-12, abs=1e-14)
+    # the ASP push path applies the same step
+    o = orc.Oracle([x0], 1, 1, eta, mu, dtype=np.float64)
+    assert o.set_lr_policy(2, 0.0) == 0       # eta_ASP = eta
+    o.set_nesterov(True)
+    o.switch(orc.ASP, 0)
+    v, x = 0.0, x0
+    for t in range(20):
+        rc, _ = o.asp_push(0, [a * o.params()[0]], t)
+        assert rc == 0
+        v, x = N @ np.array([v, x])
+        assert o.params()[0] == pytest.approx(x, rel=1e-12, abs=1e-14)
+
+
+def test_nesterov_special_cases(orc):
+    rng = np.random.default_rng(4)
+    w0 = rng.standard_normal(301).astype(np.float32)
+    gs = [rng.standard_normal(301).astype(np.float32) for _ in range(3)]
+    # mu = 0: Nesterov and the classical step coincide bit for bit (g + 0*v' = g)
+    a, b = orc.Oracle(w0, 3, 1, 0.25, 0.0), orc.Oracle(w0, 3, 1, 0.25, 0.0)
+    a.set_nesterov(True)
+    for g in gs:
+        a.bsp_step([g])
+        b.bsp_step([g])
+    assert np.array_equal(a.params(), b.params())
+    # mu > 0: the first step differs exactly by the look-ahead term eta*mu*v1 (v0 = 0, so v1 = g), fp64
+    a, b = (orc.Oracle(w0, 3, 1, 0.25, 0.5, dtype=np.float64) for _ in range(2))
+    a.set_nesterov(True)
+    a.bsp_step([gs[0]])
+    b.bsp_step([gs[0]])
+    np.testing.assert_allclose(b.params() - a.params(), 0.25 * 0.5 * gs[0].astype(np.float64), rtol=1e-12,
+                               atol=1e-15)
+    assert a.set_nesterov(2) != 0
+
+
 # ---------------------------------------------------------------------------------------------------------------
 # BSP == mini-batch SGD on the concatenated batch ("equivalent to a true mini-batch stochastic gradient
 # descent algorithm"); n = 1 special case
