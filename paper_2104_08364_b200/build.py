@@ -40,7 +40,7 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Builds the library (out/defines: tuning variants for tools/replay_sweep.py; the product is the default)."""
+    """Builds the library (out/defines: tuning variants for tools/kernel_sweep.py; the product is the default)."""
     if out is None and not (force or _stale()):
         return LIB
     inc, lib = nccl_dirs()

@@ -143,8 +143,14 @@ __device__ __forceinline__ bool is_pow2(float d) {
 
 // ---------------------------------------------------------------------------------------------------------------
 // K1 bsp_update
-constexpr int kU1 = 2;  // float4 chunks per thread per iteration
-constexpr int kG1 = 8;  // gradients loaded together
+#ifndef SS_BSP_U
+#define SS_BSP_U 2          // tuning knobs (tools/kernel_sweep.py builds variants)
+#endif
+#ifndef SS_BSP_G
+#define SS_BSP_G 8
+#endif
+constexpr int kU1 = SS_BSP_U;  // float4 chunks per thread per iteration
+constexpr int kG1 = SS_BSP_G;  // gradients loaded together
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
 // v of a tile live in registers for the whole window; thread 0 keeps kTmaStages tile loads in flight ahead of the
 // consumers, across push and tile boundaries, so the bytes in flight no longer depend on registers per thread.
 #ifndef SS_TMA_TILE
-#define SS_TMA_TILE 2048   // tuning knobs (tools/replay_sweep.py builds variants)
+#define SS_TMA_TILE 2048   // tuning knobs (tools/kernel_sweep.py builds variants)
 #endif
 #ifndef SS_TMA_STAGES
 #define SS_TMA_STAGES 10   // 80 KB rings -> 2 CTAs per SM: 96.5-98% of the HBM copy vs 93% at 6 stages / 4 CTAs
