@@ -82,8 +82,9 @@ struct ss_ctx {
   int *flag = nullptr;                 // non-finite flag
   float *sum_buf = nullptr;            // G > 1: local pre-sum [P_pad]
   float *rs_buf = nullptr;             // G > 1: reduce-scattered sum [reg_len]
-  std::vector<float *> stage;          // full-length staging slots for host pointers
-  int32_t stage_used = 0;
+  std::vector<float *> stage;          // full-length staging slots for host pointers (a ring, see stage_slot)
+  int32_t stage_next = 0;              // ring cursor once the pool is full
+  std::vector<int32_t> win_slots;      // slots taken by the pending window / superstep, released after its kernels
   // single GPU: host<->device staging copies run on their own streams so PCIe traffic in both directions overlaps
   // the kernels and each other; per-slot events order reuse (slot_free) and consumption (slot_ready)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
@@ -228,9 +229,22 @@ void record(ss_ctx *c, int64_t worker, int64_t b, int64_t st) {
   c->log.push_back(c->version);
 }
 
-ss_status stage_slot(ss_ctx *c, float **out, int32_t *index = nullptr) {
+// Staging slots form a ring: the pool grows to stage_cap() slots, then the oldest slot is reused. A slot taken for an
+// H2D waits (on copy_in) for its previous user to be done with it, a slot a kernel will write (host pull) makes the
+// compute stream wait the same way, so reuse is always ordered; the ring keeps consecutive windows on distinct slots
+// when memory allows, so the waits rarely stall. Slots are taken after any window cut (enqueue), so the slots of one
+// window or superstep are distinct as long as the pool holds max(n, window) of them.
+int32_t stage_cap(const ss_ctx *c) {
+  const int64_t need = std::max<int64_t>(c->n, c->max_win);
+  const int64_t slot_bytes = std::max<int64_t>(1, c->P_pad * (int64_t)sizeof(float));
+  const int64_t budget = (int64_t)24 << 30;   // prefer two windows' worth within 24 GB of HBM
+  return (int32_t)std::max<int64_t>(need, std::min<int64_t>(2 * need, budget / slot_bytes));
+}
+
+ss_status stage_slot(ss_ctx *c, float **out, int32_t *index, bool kernel_writes) {
   if (c->capturing) return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
-  if (c->stage_used == (int32_t)c->stage.size()) {
+  int32_t i;
+  if ((int32_t)c->stage.size() < stage_cap(c)) {
     float *p = nullptr;
     cudaEvent_t f, r;
     SS_CUDA(c, cudaMalloc(&p, (size_t)c->P_pad * sizeof(float)));
@@ -240,16 +254,22 @@ ss_status stage_slot(ss_ctx *c, float **out, int32_t *index = nullptr) {
     c->slot_free.push_back(f);
     c->slot_ready.push_back(r);
     c->slot_armed.push_back(0);
+    i = (int32_t)c->stage.size() - 1;
+  } else {
+    i = c->stage_next;
+    c->stage_next = (i + 1) % (int32_t)c->stage.size();
   }
-  if (index) *index = c->stage_used;
-  *out = c->stage[c->stage_used++];
+  if (kernel_writes && c->slot_armed[i]) SS_CUDA(c, cudaStreamWaitEvent(c->stream, c->slot_free[i], 0));
+  c->win_slots.push_back(i);
+  if (index) *index = i;
+  *out = c->stage[i];
   return SS_OK;
 }
 
-bool split_copies(const ss_ctx *c) { return c->world == 1 && c->copy_in != nullptr; }
+bool split_copies(const ss_ctx *c) { return c->copy_in != nullptr; }
 
-// Host gradient -> device staging slot (the caller's buffer is borrowed until ss_sync). Single GPU: the H2D runs on
-// copy_in after the slot's previous consumer, and the compute stream waits only for this copy.
+// Host gradient -> device staging slot (the caller's buffer is borrowed until ss_sync). The H2D runs on copy_in after
+// the slot's previous user is done with it, and the compute stream waits only for this copy.
 ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
   if (!is_host_ptr(g)) {
     *out = g;
@@ -257,7 +277,7 @@ ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
   }
   float *slot = nullptr;
   int32_t i = 0;
-  SS_TRY(stage_slot(c, &slot, &i));
+  SS_TRY(stage_slot(c, &slot, &i, false));
   if (split_copies(c)) {
     if (c->slot_armed[i]) SS_CUDA(c, cudaStreamWaitEvent(c->copy_in, c->slot_free[i], 0));
     SS_CUDA(c, cudaMemcpyAsync(slot, g, (size_t)c->P * sizeof(float), cudaMemcpyHostToDevice, c->copy_in));
@@ -270,14 +290,19 @@ ss_status resolve_src(ss_ctx *c, const float *g, const float **out) {
   return SS_OK;
 }
 
-// After the kernel that consumed slots [0, stage_used) was enqueued: they may be refilled once it is done.
-ss_status release_slots(ss_ctx *c) {
+// After the kernels that read the window's / superstep's slots were enqueued: gradient slots may be refilled once
+// they are done; a host pull's slot is released by its D2H (pull_to_host).
+ss_status release_slots(ss_ctx *c, const std::vector<Ev> *win = nullptr) {
   if (split_copies(c))
-    for (int32_t i = 0; i < c->stage_used; ++i) {
+    for (int32_t i : c->win_slots) {
+      bool pull = false;
+      if (win)
+        for (const Ev &e : *win) pull = pull || (e.kind == 1 && e.host_dst && e.slot == i);
+      if (pull) continue;
       SS_CUDA(c, cudaEventRecord(c->slot_free[i], c->stream));
       c->slot_armed[i] = 1;
     }
-  c->stage_used = 0;
+  c->win_slots.clear();
   return SS_OK;
 }
 
@@ -584,25 +609,24 @@ ss_status flush_fused(ss_ctx *c) {
   timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
   SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
   timed_end(c, &t);
+  // gradient slots are free once the kernels that read them are done (host pulls keep theirs until their D2H)
+  SS_TRY(release_slots(c, &c->win));
   for (const Ev &e : c->win) {
     if (e.kind != 1 || !e.data || host_of(c, e.worker) != me) continue;
     const float *pb = c->pbuf + (int64_t)(e.worker - c->first_hosted) * c->P_pad;
     if (e.dst == pb) continue;  // zero-copy pull into the mapped pull buffer (ss_pull_buffer)
-    if (e.host_dst)
-      SS_CUDA(c, cudaMemcpyAsync(e.host_dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-    else
-      SS_CUDA(c, cudaMemcpyAsync(e.dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    // the pull buffer is rewritten by the owners in the next window, which cannot start before this rank's next
+    // kernel: copy it out on the compute stream (into the staging slot for a host destination, whose D2H then runs
+    // on copy_out, overlapping the next window)
+    SS_CUDA(c, cudaMemcpyAsync(e.dst, pb, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    if (e.host_dst) SS_TRY(pull_to_host(c, e));
   }
   c->win.clear();
-  c->stage_used = 0;
   return SS_OK;
 }
 
 ss_status flush(ss_ctx *c) {
-  if (c->win.empty()) {
-    c->stage_used = 0;
-    return SS_OK;
-  }
+  if (c->win.empty()) return SS_OK;
   if (c->world > 1 && c->fused_mode != 0) return flush_fused(c);
   const int32_t me = c->rank;
   const int64_t lo = c->real_lo[me], hi = c->real_hi[me], cnt = hi - lo;
@@ -690,20 +714,10 @@ ss_status flush(ss_ctx *c) {
   }
 
   // slots read by the kernel (gradients) are free after it; host pulls free theirs after their D2H
-  if (split_copies(c)) {
-    std::vector<uint8_t> is_pull(c->stage_used, 0);
-    for (const Ev &e : c->win)
-      if (e.kind == 1 && e.host_dst && e.slot >= 0) is_pull[e.slot] = 1;
-    for (int32_t i = 0; i < c->stage_used; ++i)
-      if (!is_pull[i]) {
-        SS_CUDA(c, cudaEventRecord(c->slot_free[i], c->stream));
-        c->slot_armed[i] = 1;
-      }
-  }
+  SS_TRY(release_slots(c, &c->win));
   for (const Ev &e : c->win)
     if (e.kind == 1 && e.host_dst) SS_TRY(pull_to_host(c, e));
   c->win.clear();
-  c->stage_used = 0;
   return SS_OK;
 }
 
@@ -730,7 +744,10 @@ ss_status check_live(ss_ctx *c) {
   return SS_OK;
 }
 
-ss_status enqueue(ss_ctx *c, const Ev &e) {
+// Appends an event to the pending window (flushing first when the window must be cut). The event's host staging —
+// the H2D of a host gradient, the slot of a host pull destination — is set up after that cut, so a window's slots
+// all belong to it.
+ss_status enqueue(ss_ctx *c, Ev e, const float *src = nullptr, float *pull_dst = nullptr) {
   std::vector<int32_t> kd, wk;
   for (const Ev &x : c->win) {
     kd.push_back(x.kind);
@@ -739,6 +756,17 @@ ss_status enqueue(ss_ctx *c, const Ev &e) {
   if (ss::window_cut(kd.data(), wk.data(), (int32_t)kd.size(), e.kind, e.worker, c->max_win,
                      c->world > 1 && c->fused_mode != 0))
     SS_TRY(flush(c));
+  if (e.kind == 0 && src) SS_TRY(resolve_src(c, src, &e.src));
+  if (e.kind == 1 && pull_dst) {
+    if (is_host_ptr(pull_dst)) {
+      float *slot = nullptr;
+      SS_TRY(stage_slot(c, &slot, &e.slot, true));
+      e.dst = slot;
+      e.host_dst = pull_dst;
+    } else {
+      e.dst = pull_dst;
+    }
+  }
   c->win.push_back(e);
   if ((int32_t)c->win.size() >= c->max_win) return flush(c);
   return SS_OK;
@@ -1205,7 +1233,6 @@ ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t vers
   Ev e{};
   e.kind = 0;
   e.worker = worker;
-  if (mine) SS_TRY(resolve_src(c, grad, &e.src));
   e.lr = lr_at(c, c->version, SS_ASP);
   e.mu = asp_momentum(c, c->version);
   const int64_t st = c->version - version;
@@ -1213,7 +1240,7 @@ ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t vers
   c->version += 1;
   c->stepped = true;
   if (staleness_out) *staleness_out = st;
-  return enqueue(c, e);
+  return enqueue(c, e, mine ? grad : nullptr);
 }
 
 ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
@@ -1231,17 +1258,7 @@ ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
   e.worker = worker;
   e.data = c->world > 1 || dst != nullptr;
   if (!e.data) return SS_OK;
-  if (mine) {
-    if (is_host_ptr(dst)) {
-      float *slot = nullptr;
-      SS_TRY(stage_slot(c, &slot, &e.slot));
-      e.dst = slot;
-      e.host_dst = dst;
-    } else {
-      e.dst = dst;
-    }
-  }
-  return enqueue(c, e);
+  return enqueue(c, e, nullptr, mine ? dst : nullptr);
 }
 
 ss_status ss_switch(ss_ctx *c, int32_t proto, int64_t at_step) {

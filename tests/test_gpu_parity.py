@@ -297,6 +297,51 @@ def test_repeated_init_destroy(ss):
         g.close()
 
 
+@pytest.mark.parametrize("window", [2, 16])
+def test_host_buffers_full_size_slot_reuse(ss, orc, window):
+    """The e2e pattern at config 3 size: pinned host gradients and a distinct pinned host destination for every pull,
+    three ASP rounds (each push followed by its pull). Staging slots are reused across windows while earlier D2H
+    copies may still be running (window 2: every window reuses the ring); every snapshot must equal the oracle's on
+    4,096 sampled elements."""
+    P, n, S = 25_557_032, 8, 8
+    rng = np.random.default_rng(1)
+    idx = np.unique(np.concatenate([rng.choice(P, 4090, replace=False), [0, 1, P - 2, P - 1]]))
+    ti = torch.from_numpy(idx).cuda()
+    w0d = torch.empty(P, device="cuda")
+    ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0d)
+    g = ss.SyncSwitch(w0d, S, n, 0.1, 0.9)
+    g.set_window(window)
+    o = orc.Oracle(w0d[ti].cpu().numpy(), 1, n, 0.1, 0.9)
+    del w0d
+    hgrad, sgrad = {}, {}
+    for j in range(n):
+        for r in range(2):
+            d = dev_synth(ss, j, r, P)
+            hgrad[(j, r)] = torch.empty(P, pin_memory=True)
+            hgrad[(j, r)].copy_(d)
+            sgrad[(j, r)] = d[ti].cpu().numpy()
+            del d
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    base_g = {j: g.pull(j) for j in range(n)}
+    base_o = {j: o.pull(j, False)[2] for j in range(n)}
+    snaps, expected = [], []
+    for rnd in range(3):
+        for j in range(n):
+            assert g.asp_push(j, hgrad[(j, rnd % 2)], base_g[j]) == o.asp_push(j, sgrad[(j, rnd % 2)], base_o[j])[1]
+            dst = torch.empty(P, pin_memory=True)
+            base_g[j] = g.pull(j, dst)
+            rc, snap, base_o[j] = o.pull(j)
+            snaps.append(dst)
+            expected.append(snap)
+    g.sync()
+    hidx = torch.from_numpy(idx)
+    for got, want in zip(snaps, expected):
+        assert np.array_equal(got[hidx].numpy(), want)
+    assert np.array_equal(g.params()[idx], o.params())
+    g.close()
+
+
 # ---------------------------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("P", [25_557_032, 100_000_000, 1_000_000_000])
 def test_full_size_sampled(ss, orc, P):
