@@ -265,25 +265,27 @@ def run_ours(args):
     st = g.stats(64)
     assert st["status"] == 0 and g.sync_status() == 0, g.last_error()
 
-    # the same step replayed from a CUDA graph (ss_capture_*; single GPU): device launch gaps removed
-    graph = None
-    if world == 1:
-        g.capture_begin()
-        ver = step_dev(ver)
-        g.capture_end()
-        g.capture_replay(args.warmup)
-        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        ge0.record(stream)
-        g.capture_replay(args.steps)
-        ge1.record(stream)
-        torch.cuda.synchronize()
-        gms = ge0.elapsed_time(ge1)
-        assert g.sync_status() == 0, g.last_error()
-        graph = {"steps_per_s": round(args.steps / (gms / 1e3), 3), "ms_per_step": gms / args.steps,
-                 "note": "ss_capture_replay: one captured step (4 kernels) replayed; host protocol state advanced "
-                         "identically"}
-        ver = g.version
+    # the same step replayed from a CUDA graph (ss_capture_*; every rank captures and replays it): host launch
+    # overhead removed
+    g.capture_begin()
+    ver = step_dev(ver)
+    g.capture_end()
+    g.capture_replay(args.warmup)
+    ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ge0.record(stream)
+    g.capture_replay(args.steps)
+    ge1.record(stream)
+    barrier()
+    gt = torch.tensor([ge0.elapsed_time(ge1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+    gms = gt.item()
+    assert g.sync_status() == 0, g.last_error()
+    graph = {"steps_per_s": round(args.steps / (gms / 1e3), 3), "ms_per_step": gms / args.steps,
+             "note": "ss_capture_replay: one captured step replayed on every rank; host protocol state advanced "
+                     "identically"}
+    ver = g.version
 
     # e2e: same steps through the C-ABI with HOST (pinned) buffers, H2D / D2H inside the timed region
     e2e = None

@@ -233,7 +233,7 @@ ss_status ss_set_window(ss_ctx *ctx, int32_t max_events);
 ss_status ss_get_stream(ss_ctx *ctx, void **stream_out);
 /* Order the context's work after `stream` (cudaStream_t) — used when gradients are produced on another stream. */
 ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
-/* CUDA-graph capture of one step (single GPU; SV §8(d): latency-bound small models "with and without CUDA Graphs").
+/* CUDA-graph capture of one step (SV §8(d): latency-bound small models "with and without CUDA Graphs", G = 1..8).
  * Between ss_capture_begin and ss_capture_end, the calls run their host logic as usual but their device work is
  * recorded into a graph instead of executing; ss_capture_end instantiates it and launches it once (so the captured
  * step has happened on both sides) and returns the step's version delta. ss_capture_replay(K) launches the graph K
@@ -242,6 +242,9 @@ ss_status ss_wait_stream(ss_ctx *ctx, void *stream);
  * (relative base versions, no pending switch, no queued window) and nothing baked into the kernels to change over
  * the replayed versions (no lr boundary inside, momentum rule 0). Buffers the step used stay BORROWED while a
  * graph exists. Calls that allocate (first use of host buffers) must not happen during capture: warm up first.
+ * Multi-GPU: collective — every rank captures the same step and replays it the same number of times; run one
+ * ordinary step first (the exchange buffers, peer mappings and NVLS replica are set up lazily). The fused kernels'
+ * cross-GPU flag epochs come from a device-resident counter, so replays synchronise with fresh epochs.
  * Errors: SS_E_STATE, SS_E_CUDA. */
 ss_status ss_capture_begin(ss_ctx *ctx);
 ss_status ss_capture_end(ss_ctx *ctx, int64_t *version_delta);

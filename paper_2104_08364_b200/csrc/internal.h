@@ -18,9 +18,13 @@ struct PeerSync {
   uint32_t *ctr;                    // CTA completion counter (local, returns to 0 after each use)
   int *err;                         // set when a wait times out (surfaced by ss_sync as SS_E_CUDA)
   int32_t rank, world;
-  uint32_t wait_epoch;              // !=0: every CTA waits for flag >= wait_epoch from all ranks before starting
-  uint32_t signal_epoch;            // !=0: the last CTA to finish signals every rank with signal_epoch
-  int32_t end_wait;                 // and then waits until every rank has signalled signal_epoch
+  // Epochs are relative to this rank's device-resident counter *epoch_base (read at kernel entry, advanced by the last
+  // CTA to the signalled epoch), so a captured CUDA graph replays with fresh epochs every time.
+  uint32_t *epoch_base;
+  int32_t has_wait;                 // every CTA waits for flag >= base + wait_off from all ranks before starting
+  uint32_t wait_off;
+  uint32_t signal_off;              // !=0: the last CTA to finish signals every rank with base + signal_off
+  int32_t end_wait;                 // and then waits until every rank has signalled it
   unsigned long long *trace;        // SS_TRACE: CTA 0 / the last CTA record globaltimer into trace[0..3] (or null)
 };
 
@@ -119,7 +123,7 @@ struct PipeBspArgs {
   float divisor, mu, neg_eta, lam;
   int32_t nesterov;
   uint32_t *work;                // item counter (local; the last CTA resets it)
-  uint32_t epoch;                // chunk-flag epoch of this step
+  uint32_t epoch;                // chunk-flag epoch of this step, as an offset from the device epoch counter
   PeerSync sync;                 // end barrier: signal + wait
 };
 

@@ -75,19 +75,32 @@ __device__ void peer_wait(const PeerSync &s, uint32_t epoch) {
   __syncthreads();
 }
 
-// Block-wide, at kernel entry: CTA 0 stamps trace[0]; every CTA waits for wait_epoch when set (CTA 0 stamps trace[1]).
-__device__ __forceinline__ void peer_enter(const PeerSync &s) {
-  if (blockIdx.x == 0) trace_mark(s, 0);
-  if (s.wait_epoch) {
-    peer_wait(s, s.wait_epoch);
-    if (blockIdx.x == 0) trace_mark(s, 1);
-  }
+// Absolute epochs of this launch: the rank's device counter (advanced by the previous fused kernel) + the offsets.
+struct Ep {
+  uint32_t wait, signal;
+};
+__device__ __forceinline__ Ep peer_epochs(const PeerSync &s) {
+  const uint32_t b = s.epoch_base ? *reinterpret_cast<const volatile uint32_t *>(s.epoch_base) : 0u;
+  return Ep{b + s.wait_off, s.signal_off ? b + s.signal_off : 0u};
 }
 
-// Block-wide, at kernel end: the last CTA of the grid publishes signal_epoch to every rank (after a system-scope fence
-// that orders all of this grid's stores, local and remote, before the flag) and optionally waits for all ranks.
-__device__ void peer_done(const PeerSync &s) {
-  if (s.signal_epoch == 0) return;
+// Block-wide, at kernel entry: CTA 0 stamps trace[0]; every CTA waits for the wait epoch when set (CTA 0 stamps
+// trace[1]). Returns the launch's epochs.
+__device__ __forceinline__ Ep peer_enter(const PeerSync &s) {
+  const Ep ep = peer_epochs(s);
+  if (blockIdx.x == 0) trace_mark(s, 0);
+  if (s.has_wait) {
+    peer_wait(s, ep.wait);
+    if (blockIdx.x == 0) trace_mark(s, 1);
+  }
+  return ep;
+}
+
+// Block-wide, at kernel end: the last CTA of the grid publishes the signal epoch to every rank (after a system-scope
+// fence that orders all of this grid's stores, local and remote, before the flag), advances the rank's epoch counter
+// to it, and optionally waits for all ranks.
+__device__ void peer_done(const PeerSync &s, const Ep &ep) {
+  if (ep.signal == 0) return;
   __threadfence_system();
   __syncthreads();
   __shared__ uint32_t last;
@@ -98,10 +111,11 @@ __device__ void peer_done(const PeerSync &s) {
     *s.ctr = 0;
     __threadfence_system();
     trace_mark(s, 2);
-    for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, s.signal_epoch);
+    for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, ep.signal);
+    *s.epoch_base = ep.signal;   // every CTA of this grid read the base at entry; the next kernel sees the new one
   }
   if (s.end_wait) {
-    peer_wait(s, s.signal_epoch);
+    peer_wait(s, ep.signal);
     trace_mark(s, 3);
   }
 }
@@ -154,7 +168,7 @@ constexpr int kG1 = SS_BSP_G;  // gradients loaded together
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
-  peer_enter(a.sync);
+  const Ep ep = peer_enter(a.sync);
   const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
   if (a.mc_w) asm volatile("fence.proxy.alias;" ::: "memory");  // multicast stores before unicast accesses
-  peer_done(a.sync);
+  peer_done(a.sync, ep);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -299,7 +313,7 @@ constexpr int kU2 = 4;
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_constant__ AspArgs a) {
-  peer_enter(a.sync);
+  const Ep ep = peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const float lam = a.lam;
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
-  peer_done(a.sync);
+  peer_done(a.sync, ep);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -441,7 +455,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
-  peer_enter(a.sync);
+  const Ep ep = peer_enter(a.sync);
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int push_ev[kMaxEvents];
@@ -550,14 +564,14 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
-  peer_done(a.sync);
+  peer_done(a.sync, ep);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
 // scatter (fused path): every hosted gradient's owner slices go to the owners' inboxes with
 // posted 128-bit NVLink stores (the local slice is read in place by the owner update, never copied).
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
-  peer_enter(a.sync);
+  const Ep ep = peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int me = a.sync.rank, G = a.sync.world;
@@ -584,7 +598,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
       if (i < cnt) dst[i] = src[i];
     }
   }
-  peer_done(a.sync);
+  peer_done(a.sync, ep);
 }
 
 // scatter_sum (fused mode 2): one pass over the hosted gradients — sum them in ascending order and store each owner's
@@ -593,7 +607,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 // stores to every peer and the local-only pass over the own region run at the same time (processing the regions one
 // after another left the own region's HBM pass on the critical path after the NVLink-bound ones).
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
-  peer_enter(a.sync);
+  const Ep ep = peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
   const int k = (int)(blockIdx.x % G);
   const int64_t n_cta = ((int64_t)gridDim.x - k + G - 1) / G;             // CTAs in subset k
@@ -636,7 +650,7 @@ __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_cons
     for (int j = 1; j < a.n_src; ++j) acc = __fadd_rn(acc, a.src[j][lo + i]);
     dst[i] = acc;
   }
-  peer_done(a.sync);
+  peer_done(a.sync, ep);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -660,6 +674,8 @@ __device__ __forceinline__ void chunk_copy(float *dst, const float *src, int64_t
 
 __global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constant__ PipeBspArgs a) {
   __shared__ uint32_t s_item;
+  const Ep ep = peer_epochs(a.sync);
+  const uint32_t chunk_epoch = ep.signal - a.sync.signal_off + a.epoch;   // base + the chunk-flag offset
   const int me = a.sync.rank, G = a.sync.world;
   const uint32_t nA = (uint32_t)(G * a.max_chunks);
   const uint32_t nB = (uint32_t)a.n_chunks[me];
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constan
       }
       __threadfence_system();
       __syncthreads();
-      if (threadIdx.x == 0) st_release_sys(a.flags[q] + c * kMaxPeers + me, a.epoch);
+      if (threadIdx.x == 0) st_release_sys(a.flags[q] + c * kMaxPeers + me, chunk_epoch);
     } else {
       // ---------------- phase B: chunk c of this rank's region ----------------
       const int c = (int)(it - nA);
@@ -707,7 +723,7 @@ __global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constan
         for (int q = 0; q < G; ++q) {
           if (q == me && !a.presum) continue;
           const uint32_t *f = a.flags[me] + c * kMaxPeers + q;
-          while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+          while ((int32_t)(ld_acquire_sys(f) - chunk_epoch) < 0) {
             if (globaltimer() - t0 > kTimeoutNs) {
               atomicExch(a.sync.err, 1);
               break;
@@ -768,9 +784,10 @@ __global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constan
     a.work[0] = 0;
     a.work[1] = 0;
     __threadfence_system();
-    for (int q = 0; q < G; ++q) st_release_sys(a.sync.sig_peer[q] + me, a.sync.signal_epoch);
+    for (int q = 0; q < G; ++q) st_release_sys(a.sync.sig_peer[q] + me, ep.signal);
+    *a.sync.epoch_base = ep.signal;
   }
-  peer_wait(a.sync, a.sync.signal_epoch);
+  peer_wait(a.sync, ep.signal);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -988,7 +1005,7 @@ int grid_for(K kernel, int64_t work_items) {
 }  // namespace
 
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
-  if (a.count <= 0 && a.sync.wait_epoch == 0 && a.sync.signal_epoch == 0) return cudaSuccess;
+  if (a.count <= 0 && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
   if (vec) {
     auto k = bsp_update_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
@@ -1012,7 +1029,7 @@ cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
 }
 
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
-  if ((a.count <= 0 || a.n_ev <= 0) && a.sync.wait_epoch == 0 && a.sync.signal_epoch == 0) return cudaSuccess;
+  if ((a.count <= 0 || a.n_ev <= 0) && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
   static const int variant = [] {  // SS_ASP_KERNEL=reg selects the register-prefetch form (A/B measurement)
     const char *e = getenv("SS_ASP_KERNEL");
     return (e && e[0] == 'r') ? 0 : 1;

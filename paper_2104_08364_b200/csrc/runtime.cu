@@ -112,7 +112,7 @@ struct ss_ctx {
   int64_t inbox_slots = 0;
   float *inbox = nullptr;              // [inbox_slots][reg_len] gradient slices owned here, written by peers
   float *pbuf = nullptr;               // [n_hosted][P_pad] pull buffers of hosted workers, written by owners
-  uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag
+  uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag, [96..] pipe work, [160] epoch counter
   float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
   uint32_t *peer_sig[ss::kMaxPeers] = {};
   std::vector<void *> opened;          // peer mappings to close
@@ -121,12 +121,14 @@ struct ss_ctx {
   bool w_vmm = false;                  // w points into the NVLS replica (not cudaMalloc memory)
   char job_tag[48] = {0};              // names the NVLS fd socket: hash of the NCCL unique id + setup count
   uint32_t epoch = 0;
+  uint32_t dev_epoch = 0;              // host mirror of the device epoch counter sigblk[kSigEpochBase] (peer_sync)
   int32_t first_hosted = 0, n_hosted = 0;
   // CUDA-graph capture of one step (ss_capture_*): device work + the host-state deltas it produced
   bool capturing = false;
   cudaGraphExec_t graph = nullptr;
   int64_t cap_v0 = 0, cap_dv = 0, cap_log0 = 0, cap_rel_since = 0;
   uint64_t cap_ddropped = 0;
+  uint32_t cap_epoch0 = 0, cap_depoch = 0;   // fused-path flag epochs consumed by the captured step
   std::vector<int64_t> cap_base0, cap_log;   // log records appended during the captured step
   // instrumentation
   unsigned long long *trace_dev = nullptr;   // SS_TRACE=<prefix>: 4 globaltimer stamps per fused launch
@@ -508,6 +510,8 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   return SS_OK;
 }
 
+constexpr int kSigEpochBase = 160;   // sigblk word: this rank's epoch counter, advanced by the fused kernels
+
 ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bool end_wait, int kind) {
   ss::PeerSync p;
   std::memset(&p, 0, sizeof p);
@@ -521,8 +525,13 @@ ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bo
   p.err = reinterpret_cast<int *>(c->sigblk + 64);
   p.rank = c->rank;
   p.world = c->world;
-  p.wait_epoch = wait_epoch;
-  p.signal_epoch = signal_epoch;
+  // epochs travel as offsets from the device-resident counter (kSigEpochBase), whose value before this launch the
+  // host mirrors in dev_epoch: identical to absolute epochs eagerly, and still correct when a graph is replayed
+  p.epoch_base = c->sigblk + kSigEpochBase;
+  p.has_wait = wait_epoch != 0;
+  p.wait_off = wait_epoch - c->dev_epoch;
+  p.signal_off = signal_epoch ? signal_epoch - c->dev_epoch : 0u;
+  if (signal_epoch) c->dev_epoch = signal_epoch;
   p.end_wait = end_wait ? 1 : 0;
   return p;
 }
@@ -1106,7 +1115,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     pa.lam = a.lam;
     pa.nesterov = a.nesterov;
     pa.work = c->sigblk + 96;
-    pa.epoch = epA;
+    pa.epoch = epA - c->dev_epoch;   // chunk-flag epoch as an offset from the device counter (see peer_sync)
     pa.sync = peer_sync(c, 0, epB, true, 4);
     Timed t;
     const double cnt_me = (double)(c->real_hi[me] - lo);
@@ -1296,8 +1305,13 @@ ss_status ss_sync(ss_ctx *c) {
 // the host-state deltas the step produced (versions, base versions, staleness records, drops) K times.
 ss_status ss_capture_begin(ss_ctx *c) {
   SS_TRY(check_live(c));
-  if (c->world > 1) return fail(c, SS_E_STATE, "graph capture is single-GPU (the fused path's flag epochs change)");
   if (c->capturing || c->prof) return fail(c, SS_E_STATE, "already capturing, or profiling is on");
+  // G > 1: the exchange buffers, peer mappings and NVLS replica are set up by the first step (allocation and
+  // synchronisation cannot be captured); the fused kernels take their flag epochs from a device counter, so the
+  // graph replays with fresh epochs on every rank
+  if (c->world > 1 && (c->fused_mode != 0 ? !c->ipc_ready : (c->sum_buf == nullptr ||
+                                                              (int32_t)c->rslot.size() < c->max_win)))
+    return fail(c, SS_E_STATE, "run one ordinary step before capturing (multi-GPU buffers are set up lazily)");
   SS_TRY(flush(c));
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
@@ -1308,6 +1322,7 @@ ss_status ss_capture_begin(ss_ctx *c) {
   c->cap_log0 = (int64_t)c->log.size();
   c->cap_ddropped = c->dropped;
   c->cap_rel_since = c->version - c->asp_since;
+  c->cap_epoch0 = c->epoch;
   SS_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
   return SS_OK;
@@ -1327,6 +1342,7 @@ ss_status ss_capture_end(ss_ctx *c, int64_t *version_delta) {
   // the captured step already ran on the host side; its device work has not: run it once now
   SS_CUDA(c, cudaGraphLaunch(c->graph, c->stream));
   c->cap_dv = c->version - c->cap_v0;
+  c->cap_depoch = c->epoch - c->cap_epoch0;
   c->cap_log.assign(c->log.begin() + c->cap_log0, c->log.end());
   c->cap_ddropped = c->dropped - c->cap_ddropped;
   if (version_delta) *version_delta = c->cap_dv;
@@ -1361,6 +1377,8 @@ ss_status ss_capture_replay(ss_ctx *c, int64_t times) {
       c->log.push_back(c->cap_log[i + 3] + shift + dv);
     }
     c->version += dv;
+    c->epoch += c->cap_depoch;         // the replayed kernels advanced the device epoch counter by as much
+    c->dev_epoch += c->cap_depoch;
     for (auto &b : c->base) b += dv;
     c->dropped += c->cap_ddropped;
     if (c->asp_since >= c->cap_v0) c->asp_since += dv;   // the step switched to ASP: so does every replay

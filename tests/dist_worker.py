@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--host-buffers", type=int, default=0, help="gradients and pull destinations in host memory")
     ap.add_argument("--scenario", type=int, default=-1, help="run ss_scenario_run with this policy instead")
     ap.add_argument("--nesterov", type=int, default=0)
+    ap.add_argument("--capture", type=int, default=-1,
+                    help="bench step (BSP + switch + n push/pull + switch) once, captured once, replayed this often")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -91,6 +93,36 @@ def main():
         np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=g.params(), v=g.velocity(), log=np.array(log),
                  res=np.array([res[k] for k in ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version")]),
                  hist=st["hist"], plog=g.log())
+        g.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+
+    if a.capture >= 0:
+        g.set_lr_schedule([1 << 40], [0.5])       # no lr boundary inside the replayed versions
+        bsp_g = {j: grad(j) for j in range(n)}
+        asp_g = {j: grad(j) for j in range(n)}
+        dst = {j: torch.empty(P, device="cuda") for j in hosted}
+
+        def step():
+            v = g.version
+            g.bsp_step([bsp_g[j] for j in hosted], hosted, [v] * len(hosted))
+            g.switch(ss.SS_ASP, 0)
+            for j in range(n):
+                assert g.asp_push(j, asp_g[j], v + 1) == j
+                g.pull(j, dst.get(j))
+            g.switch(ss.SS_BSP, 0)
+
+        step()
+        g.capture_begin()
+        step()
+        assert g.capture_end() == 1 + n
+        g.capture_replay(a.capture)
+        g.sync()
+        st = g.stats(64)
+        np.savez(os.path.join(a.out, f"rank{rank}.npz"), w=g.params(), v=g.velocity(), log=g.log(), hist=st["hist"],
+                 version=st["version"], snaps=np.stack([dst[j].cpu().numpy() for j in hosted]) if hosted else
+                 np.zeros((0, P), np.float32), hosted=np.array(hosted))
         g.close()
         dist.barrier()
         dist.destroy_process_group()

@@ -222,6 +222,42 @@ def test_multi_gpu_nvls_forced(orc, world, fused, P):
 
 
 @pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [0, 1, 2])
+def test_multi_gpu_graph_capture(orc, world, fused):
+    """ss_capture_* at G > 1 (SURVEY §8(d) config 2 "with and without CUDA Graphs"): the bench step captured once and
+    replayed 6 times on every rank equals 8 ordinary steps of the oracle — the fused kernels' flag epochs come from a
+    device counter, so every replay synchronises afresh. Bit-exact in fused-exact mode, C13 otherwise."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S, R = 464_154, 8, 8, 6
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 2 * n, "--fused", fused,
+                       "--capture", R], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    o.set_lr_schedule([1 << 40], [0.5])            # dist_worker's capture mode: no boundary in range
+    bsp_h = [orc.synth_grad(SEED, j, 0, 0, P) for j in range(n)]
+    asp_h = [orc.synth_grad(SEED, j, 1, 0, P) for j in range(n)]
+    snaps = {}
+    for _ in range(R + 2):
+        v = o.version
+        assert o.bsp_step(bsp_h, versions=[v] * n) == 0
+        o.switch(orc.ASP, 0)
+        for j in range(n):
+            assert o.asp_push(j, asp_h[j], v + 1) == (0, j)
+            snaps[j] = o.pull(j)[1]
+        o.switch(orc.BSP, 0)
+    cmp = np.array_equal if fused == 1 else close_c13
+    for r in res:
+        assert int(r["version"]) == o.version == (R + 2) * (1 + n)
+        assert np.array_equal(r["log"], o.log()) and np.array_equal(r["hist"], o.stats(64)["hist"])
+        assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
+        for j, snap in zip(r["hosted"], r["snaps"]):
+            assert cmp(snap, snaps[int(j)])
+
+
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("fused", [0, 1])
 def test_multi_gpu_host_buffers(orc, world, fused):
     """The e2e path at G > 1: gradients and pull destinations in pinned host memory (staged by the library) —
