@@ -266,25 +266,30 @@ def run_ours(args):
     assert st["status"] == 0 and g.sync_status() == 0, g.last_error()
 
     # the same step replayed from a CUDA graph (ss_capture_*; every rank captures and replays it): host launch
-    # overhead removed
-    g.capture_begin()
-    ver = step_dev(ver)
-    g.capture_end()
-    g.capture_replay(args.warmup)
-    ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    ge0.record(stream)
-    g.capture_replay(args.steps)
-    ge1.record(stream)
-    barrier()
-    gt = torch.tensor([ge0.elapsed_time(ge1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
-    gms = gt.item()
-    assert g.sync_status() == 0, g.last_error()
-    graph = {"steps_per_s": round(args.steps / (gms / 1e3), 3), "ms_per_step": gms / args.steps,
-             "note": "ss_capture_replay: one captured step replayed on every rank; host protocol state advanced "
-                     "identically"}
+    # overhead removed. Informational (single GPU: faster for latency-bound configs; G > 1: the replayed fused kernels
+    # run slower than the eager ones, profiles/r01_summary.md), so a failure here does not cost the line.
+    graph = None
+    try:
+        g.capture_begin()
+        ver = step_dev(ver)
+        g.capture_end()
+        g.capture_replay(args.warmup)
+        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        ge0.record(stream)
+        g.capture_replay(args.steps)
+        ge1.record(stream)
+        barrier()
+        gt = torch.tensor([ge0.elapsed_time(ge1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gms = gt.item()
+        assert g.sync_status() == 0, g.last_error()
+        graph = {"steps_per_s": round(args.steps / (gms / 1e3), 3), "ms_per_step": gms / args.steps,
+                 "note": "ss_capture_replay: one captured step replayed on every rank; host protocol state advanced "
+                         "identically"}
+    except Exception as exc:          # noqa: BLE001 — reported, not fatal
+        graph = {"error": str(exc)[:200]}
     ver = g.version
 
     # e2e: same steps through the C-ABI with HOST (pinned) buffers, H2D / D2H inside the timed region

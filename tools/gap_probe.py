@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--prof", type=int, default=0)
     ap.add_argument("--fused", type=int, default=2)
+    ap.add_argument("--graph", type=int, default=0, help="time replays of one captured step instead")
     a = ap.parse_args()
     world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -78,11 +79,22 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0.record(stream)
     import time
-    h0 = time.perf_counter()
-    for _ in range(a.steps):
+    if a.graph:
+        g.capture_begin()
         ver = step(ver)
+        g.capture_end()
+        g.capture_replay(20)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    e0.record(stream)
+    h0 = time.perf_counter()
+    if a.graph:
+        g.capture_replay(a.steps)
+    else:
+        for _ in range(a.steps):
+            ver = step(ver)
     host_us = 1e6 * (time.perf_counter() - h0) / a.steps
     e1.record(stream)
     torch.cuda.synchronize()
@@ -91,7 +103,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        print(f"config {a.config} G={world} fused={a.fused} prof={a.prof}: {t.item():.2f} us/step "
+        print(f"config {a.config} G={world} fused={a.fused} prof={a.prof} graph={a.graph}: {t.item():.2f} us/step "
               f"(host issue {host_us:.2f} us/step on rank 0)", flush=True)
     g.close()
     if world > 1:
