@@ -290,6 +290,10 @@ def run_ours(args):
                          "identically"}
     except Exception as exc:          # noqa: BLE001 — reported, not fatal
         graph = {"error": str(exc)[:200]}
+        try:
+            g.capture_end()           # leave capture mode if the failure happened inside it
+        except Exception:             # noqa: BLE001
+            pass
     ver = g.version
 
     # e2e: same steps through the C-ABI with HOST (pinned) buffers, H2D / D2H inside the timed region
