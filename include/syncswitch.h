@@ -13,8 +13,8 @@
  *    final when the call returns. Device data movement is stream-ordered on the context's stream and may be
  *    batched lazily (ASP windows); it is complete after ss_sync().
  *  - Pointers documented "host or device" may point to device memory (cudaMalloc / torch CUDA tensors), pinned or
- *    pageable host memory; host data is staged through device buffers (single GPU: on dedicated H2D / D2H copy
- *    streams ordered by events, so transfers in both directions overlap the kernels).
+ *    pageable host memory; host data is staged through a ring of device buffers on dedicated H2D / D2H copy streams
+ *    ordered by events, so transfers in both directions overlap the kernels.
  *  - Buffers passed to a call are BORROWED until the next ss_sync() returns (the library may read/write them
  *    lazily); params passed to ss_init are COPIED. The caller keeps ownership of every buffer it passes.
  *  - A context is not thread-safe: one thread per context, calls in program order.

@@ -85,7 +85,7 @@ struct ss_ctx {
   std::vector<float *> stage;          // full-length staging slots for host pointers (a ring, see stage_slot)
   int32_t stage_next = 0;              // ring cursor once the pool is full
   std::vector<int32_t> win_slots;      // slots taken by the pending window / superstep, released after its kernels
-  // single GPU: host<->device staging copies run on their own streams so PCIe traffic in both directions overlaps
+  // host<->device staging copies run on their own streams so PCIe traffic in both directions overlaps
   // the kernels and each other; per-slot events order reuse (slot_free) and consumption (slot_ready)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> slot_free, slot_ready;
