@@ -1032,6 +1032,10 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     if (versions[i] != c->version)
       return fail(c, SS_E_BARRIER, "worker %d base version %lld != current %lld", workers[i],
                   (long long)versions[i], (long long)c->version);
+  if (c->world > 1 && c->fused_mode != 0)   // checked before any state changes (host buffers are staged aligned)
+    for (int32_t i = 0; i < n_local; ++i)
+      if (!aligned16(grads[i]) && !is_host_ptr(grads[i]))
+        return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
   SS_TRY(flush(c));
   c->stepped = true;
 
@@ -1239,6 +1243,8 @@ ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t vers
   }
   if (version > c->version || version < 0)
     return fail(c, SS_E_CAUSALITY, "base version %lld > current %lld", (long long)version, (long long)c->version);
+  if (mine && c->world > 1 && c->fused_mode != 0 && !aligned16(grad) && !is_host_ptr(grad))
+    return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
   Ev e{};
   e.kind = 0;
   e.worker = worker;
