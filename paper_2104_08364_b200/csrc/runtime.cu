@@ -239,8 +239,8 @@ void record(ss_ctx *c, int64_t worker, int64_t b, int64_t st) {
 int32_t stage_cap(const ss_ctx *c) {
   const int64_t need = std::max<int64_t>(c->n, c->max_win);
   const int64_t slot_bytes = std::max<int64_t>(1, c->P_pad * (int64_t)sizeof(float));
-  const int64_t budget = (int64_t)24 << 30;   // prefer two windows' worth within 24 GB of HBM
-  return (int32_t)std::max<int64_t>(need, std::min<int64_t>(2 * need, budget / slot_bytes));
+  const int64_t budget = (int64_t)24 << 30;   // prefer a whole step's worth (BSP gradients + ASP pushes and pulls)
+  return (int32_t)std::max<int64_t>(need, std::min<int64_t>(4 * need, budget / slot_bytes));
 }
 
 ss_status stage_slot(ss_ctx *c, float **out, int32_t *index, bool kernel_writes) {
