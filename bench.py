@@ -38,6 +38,8 @@ CONFIGS = {
     "5b": dict(P=250_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=2.5e8 fp32, n=S=8"),
     "5c": dict(P=500_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=5e8 fp32, n=S=8"),
     "5d": dict(P=1_000_000_000, n=8, S=8, window=16, name="config5: large-model sync, P=1e9 fp32, n=S=8"),
+    "1": dict(P=8192, n=2, S=2, window=1, name="config1: toy softmax regression (d=1024 incl. bias, C=8, P=8,192), "
+              "2 workers, 2 shards, 1,000 points, W=100 B, switch BSP->ASP at 50% (25 BSP steps + 50 ASP pushes)"),
     "4": dict(P=25_557_032, n=8, S=8, window=16, name="config4: ASP straggler scenario, worker 7 4x slow for "
               "100,000 ticks during BSP, greedy switching (P:1421), P=25,557,032, n=S=8"),
 }
@@ -446,6 +448,97 @@ def run_scenario(args):
 
 
 # ------------------------------------------------------------------------------------------------------------------
+def run_toy(args):
+    """Config 1 (BASELINE configs[0]): the toy model trained through the library on 1 GPU — every update's gradient
+    comes from the hand-written softmax_grad kernel on the worker's own pull (window 1: each pull is written before
+    the gradient kernel reads it, all on the library's stream, no host synchronisation inside a run). W = 100 B
+    samples switched at s = 0.5 (Table I: 25 BSP supersteps + 50 ASP pushes), seeded jittered schedule. A step = one
+    whole training run from w = 0; value = protocol updates/s including the gradient kernels."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from inputs import minibatch_order, toy_dataset
+    from paper_2104_08364_b200 import syncswitch as ss
+    cfg = CONFIGS["1"]
+    n, S, B, d, C = cfg["n"], cfg["S"], 16, 1024, 8
+    P = d * C
+    X, y = toy_dataset(seed=1)                 # the SURVEY §8(d) recipe (separable classes, eta 0.1, mu 0.9)
+    s_, (bsp_steps, asp_pushes, _) = ss.ss_table1(100 * B, B, n, 1, 2, [])
+    ss.ss_check(s_)
+    order = minibatch_order(1, len(X), n * bsp_steps + asp_pushes, B)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    Xb = [Xd[torch.from_numpy(order[b]).cuda()].contiguous() for b in range(len(order))]   # input pipeline
+    yb = [yd[torch.from_numpy(order[b]).cuda()].contiguous() for b in range(len(order))]
+    s_, (kind, worker, _) = ss.ss_schedule(n, [1000] * n, asp_pushes, jitter=100, seed=7)
+    ss.ss_check(s_)
+    losses = torch.zeros(bsp_steps * n + asp_pushes, device="cuda")
+    grads = [torch.empty(P, device="cuda") for _ in range(max(n, 1))]
+    snap = {j: torch.empty(P, device="cuda") for j in range(n)}
+    L = ss.lib
+
+    def one_run():
+        g = ss.SyncSwitch(torch.zeros(P, device="cuda"), S, n, 0.1, 0.9)
+        g.set_window(1)
+        g.switch(ss.SS_ASP, bsp_steps)
+        st = g.stream
+        mb, li = 0, 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream = torch.cuda.ExternalStream(st)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(bsp_steps):
+            g.pull(0, snap[0])
+            for j in range(n):
+                ss.ss_check(L.ss_softmax_grad(ss.ptr(Xb[mb]), ss.ptr(yb[mb]), B, d, C, ss.ptr(snap[0]),
+                                              ss.ptr(grads[j]), losses.data_ptr() + 4 * li, ctypes.c_void_p(st)))
+                mb, li = mb + 1, li + 1
+            g.bsp_step(grads[:n])
+        base = {}
+        for kd, j in zip(kind, worker):
+            j = int(j)
+            if kd == 1:
+                base[j] = g.pull(j, snap[j])
+            else:
+                ss.ss_check(L.ss_softmax_grad(ss.ptr(Xb[mb]), ss.ptr(yb[mb]), B, d, C, ss.ptr(snap[j]),
+                                              ss.ptr(grads[0]), losses.data_ptr() + 4 * li, ctypes.c_void_p(st)))
+                mb, li = mb + 1, li + 1
+                g.asp_push(j, grads[0], base[j])
+        e1.record(stream)
+        g.sync()
+        ms = e0.elapsed_time(e1)
+        st_ = g.stats(64)
+        g.close()
+        return ms, st_
+
+    for _ in range(max(args.warmup, 1)):
+        one_run()
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    runs = [one_run() for _ in range(args.steps)]
+    clk = clocks.stop()
+    ms = sum(r[0] for r in runs)
+    updates = (bsp_steps + asp_pushes) * args.steps
+    lv = losses.cpu().numpy()
+    st = runs[-1][1]
+    line = {"metric": METRIC, "value": round(updates / (ms / 1e3), 1),
+            "unit": "protocol updates/s (BSP supersteps + ASP pushes, each with its softmax_grad kernel(s))",
+            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Gaussian-mixture toy dataset, inputs/toy_dataset)",
+            "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "batch": B,
+                       "bsp_steps": bsp_steps, "asp_pushes": asp_pushes, "asp_window_events": 1,
+                       "note": "a step = one whole training run from w = 0"},
+            "training": {"loss_first": float(lv[0]), "loss_last10_mean": float(lv[-10:].mean()),
+                         "loss_every_10th_update": [round(float(x), 5) for x in lv[::10]],
+                         "version": st["version"], "staleness_hist": {str(i): int(x) for i, x in enumerate(st["hist"])
+                                                                      if x}},
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------------------------
 # --workload: sync-only time of the whole 64K-iteration training workload (SURVEY §8(d) config 2 / 3; the sync-path
 # analog of Table II's throughput column, P:1700-1740): pure BSP, pure ASP and switched at s, each with the Table I
 # workload-preserving remap of steps and lr-decay boundaries (P:296-308, DESIGN reading C11).
@@ -695,6 +788,8 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.config == "4":
         run_scenario(a)
+    elif a.config == "1":
+        run_toy(a)
     elif a.workload:
         run_workload(a)
     else:
