@@ -74,6 +74,7 @@ struct AspArgs {
   int *flag;
   int64_t count;
   int32_t n_ev;
+  int32_t tile;       // TMA form: floats per tile (multiple of 32, <= kTmaTile); set by launch_asp_replay
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;

@@ -419,6 +419,9 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
 #ifndef SS_TMA_TILE
 #define SS_TMA_TILE 2048   // tuning knobs (tools/kernel_sweep.py builds variants)
 #endif
+#ifndef SS_TMA_BALANCE
+#define SS_TMA_BALANCE 0
+#endif
 #ifndef SS_TMA_STAGES
 #define SS_TMA_STAGES 10   // 80 KB rings -> 2 CTAs per SM: 96.5-98% of the HBM copy vs 93% at 6 stages / 4 CTAs
 #endif                     // (profiles/r01_replay_sweep.txt)
@@ -472,14 +475,15 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   __syncthreads();
   const int n_push = n_push_s;
   const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
-  const int64_t n_tiles = (nvec + kTmaTile - 1) / kTmaTile;
+  const int64_t tsz = a.tile;                                // floats per tile (<= kTmaTile)
+  const int64_t n_tiles = (nvec + tsz - 1) / tsz;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * n_push;                   // one gradient tile per (tile, push)
 
   auto issue = [&](int64_t it) {                             // thread 0: stage the gradient tile of item `it`
     const int64_t tile = blockIdx.x + (it / n_push) * gridDim.x;
-    const int64_t off = tile * kTmaTile;
-    const int64_t len = min((int64_t)kTmaTile, nvec - off);
+    const int64_t off = tile * tsz;
+    const int64_t len = min(tsz, nvec - off);
     const int s = (int)(it % kTmaStages);
     mbar_expect_tx(&full[s], (uint32_t)(len * 4));
     bulk_g2s(ring + s * kTmaTile, a.ev[push_ev[it % n_push]].src + off, (uint32_t)(len * 4), &full[s]);
@@ -490,8 +494,8 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   bool bad = false;
   int64_t it = 0;
   for (int64_t tl = 0; tl < my_tiles; ++tl) {
-    const int64_t off = (blockIdx.x + tl * gridDim.x) * kTmaTile;
-    const int64_t len = min((int64_t)kTmaTile, nvec - off);
+    const int64_t off = (blockIdx.x + tl * gridDim.x) * tsz;
+    const int64_t len = min(tsz, nvec - off);
     float4 wv[kTU], vv[kTU];
     bool ok[kTU];
 #pragma unroll
@@ -1042,12 +1046,21 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k, kThreads, kTmaSmem);
       return res > 0 ? res : 1;
     }();
-    // Fixed 2048-float tiles, grid-stride over all resident CTAs. (Balancing the last wave with tiles sized to whole
-    // waves measured slower at configs 2, 3 and 5d: 337 vs 333 us at config 3.)
-    const int64_t tiles = ((a.count >> 2) * 4 + kTmaTile - 1) / kTmaTile;
-    int64_t grid = (int64_t)r * num_sms();
-    if (tiles < grid) grid = tiles > 0 ? tiles : 1;
-    k<<<(int)grid, kThreads, kTmaSmem, s>>>(a);
+    // Grid-stride over all resident CTAs. Default: fixed kTmaTile tiles. SS_TMA_BALANCE=1 (tuning build): tiles
+    // sized so the range splits into whole waves (whole 128-B lines), leaving no partly idle last wave.
+    const int64_t nvec = (a.count >> 2) << 2;
+    const int64_t slots = (int64_t)r * num_sms();
+    int64_t tile = kTmaTile;
+#if SS_TMA_BALANCE
+    const int64_t waves = std::max<int64_t>(1, (nvec + slots * kTmaTile - 1) / (slots * kTmaTile));
+    tile = std::min<int64_t>(kTmaTile, std::max<int64_t>(256, ((nvec + slots * waves - 1) / (slots * waves) + 31) &
+                                                                    ~(int64_t)31));
+#endif
+    const int64_t tiles = (nvec + tile - 1) / tile;
+    const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
+    AspArgs b = a;
+    b.tile = (int32_t)tile;
+    k<<<(int)grid, kThreads, kTmaSmem, s>>>(b);
   } else if (vec) {
     auto k = asp_replay_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);
