@@ -465,6 +465,9 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   __shared__ int n_push_s;
   const float lam = a.lam;
   if (threadIdx.x == 0) {
+    // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
+    // (generic proxy): order them after the acquire
+    if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
     int np = 0;
     for (int e = 0; e < a.n_ev; ++e)
       if (a.ev[e].kind == 0) push_ev[np++] = e;
