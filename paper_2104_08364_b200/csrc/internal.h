@@ -75,6 +75,8 @@ struct AspArgs {
   int64_t count;
   int32_t n_ev;
   int32_t tile;       // TMA form: floats per tile (multiple of 32, <= kTmaTile); set by launch_asp_replay
+  int32_t n_push;     // TMA form: number of push events and their indices in window order (set by the launcher)
+  uint8_t push_ev[kMaxEvents];
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;

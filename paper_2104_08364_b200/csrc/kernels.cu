@@ -457,26 +457,26 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// kRefill = false: every CTA's items (tiles x pushes) fit the ring, so no stage is ever reused and the per-push CTA
+// barrier is dropped (small P; a separate instantiation because a runtime-conditional barrier costs the large-P
+// loop 2.5%: profiles/r01_replay_condsync.txt).
+template <bool kRefill>
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
   const Ep ep = peer_enter(a.sync);
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ int push_ev[kMaxEvents];
-  __shared__ int n_push_s;
   const float lam = a.lam;
+  if (threadIdx.x < a.n_push) push_ev[threadIdx.x] = a.push_ev[threadIdx.x];
   if (threadIdx.x == 0) {
     // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
     // (generic proxy): order them after the acquire
     if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
-    int np = 0;
-    for (int e = 0; e < a.n_ev; ++e)
-      if (a.ev[e].kind == 0) push_ev[np++] = e;
-    n_push_s = np;
     for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int n_push = n_push_s;
+  const int n_push = a.n_push;                               // push events in window order (a.push_ev)
   const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
   const int64_t tsz = a.tile;                                // floats per tile (<= kTmaTile)
   const int64_t n_tiles = (nvec + tsz - 1) / tsz;
@@ -528,10 +528,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
             wp[c] = __fmaf_rn(neg_eta, a.nesterov ? __fmaf_rn(mu, vp[c], gg) : vp[c], wp[c]);
           }
         }
-        __syncthreads();                                        // every thread is done with stage s
-        if (threadIdx.x == 0 && it + kTmaStages < items) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(it + kTmaStages);
+        if (kRefill) {                                          // (a window that fits the ring never reuses a
+          __syncthreads();                                      // stage) every thread is done with stage s
+          if (threadIdx.x == 0 && it + kTmaStages < items) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(it + kTmaStages);
+          }
         }
         ++it;
       } else if (a.ev[e].dst != nullptr) {
@@ -1042,11 +1044,11 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     return (e && e[0] == 'r') ? 0 : 1;
   }();
   if (vec && variant == 1) {
-    auto k = asp_replay_tma_kernel;
-    static const int r = [k] {   // resident CTAs per SM at this kernel's shared memory (thread-safe static init)
+    static const int r = [] {    // resident CTAs per SM at this kernel's shared memory (thread-safe static init)
       int res = 0;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k, kThreads, kTmaSmem);
+      cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, asp_replay_tma_kernel<true>, kThreads, kTmaSmem);
       return res > 0 ? res : 1;
     }();
     // Grid-stride over all resident CTAs. Default: fixed kTmaTile tiles. SS_TMA_BALANCE=1 (tuning build): tiles
@@ -1063,7 +1065,14 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
     AspArgs b = a;
     b.tile = (int32_t)tile;
-    k<<<(int)grid, kThreads, kTmaSmem, s>>>(b);
+    b.n_push = 0;
+    for (int e = 0; e < a.n_ev; ++e)
+      if (a.ev[e].kind == 0) b.push_ev[b.n_push++] = (uint8_t)e;
+    const int64_t items = (tiles + grid - 1) / grid * b.n_push;   // most gradient tiles any CTA stages
+    if (items > kTmaStages)
+      asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
+    else
+      asp_replay_tma_kernel<false><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
   } else if (vec) {
     auto k = asp_replay_kernel<true>;
     k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);

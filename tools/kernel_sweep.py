@@ -3,8 +3,7 @@
 
     python tools/kernel_sweep.py build <set>            # here: tools/variants/<set>_<tag>.so
     python tools/kernel_sweep.py run <set> [--config 3] # on the GPU: bench.py per variant
-Sets: replay (asp_replay_tma_kernel tile x stages; profiles/r01_replay_sweep.txt), bsp (bsp_update float4 per
-thread x gradients loaded together).
+Sets: replay (asp_replay_tma_kernel tile x stages; profiles/r01_replay_sweep.txt), bsp (bsp_update float4 per thread x gradients loaded together).
 """
 import json
 import os
@@ -25,6 +24,15 @@ def tag(d):
     return "_".join(f"{k.split('_')[-1]}{v}" for k, v in d.items())
 
 
+def variants(name):
+    """Distinct variants of a set (a set may list one twice to interleave repeated runs on the same box)."""
+    out = []
+    for d in SETS[name]:
+        if d not in out:
+            out.append(d)
+    return out
+
+
 def path(name, d):
     return os.path.join(OUT, f"{name}_{tag(d)}.so")
 
@@ -33,7 +41,7 @@ def build(name):
     sys.path.insert(0, ROOT)
     from paper_2104_08364_b200.build import build as b
     os.makedirs(OUT, exist_ok=True)
-    for d in SETS[name]:
+    for d in variants(name):
         b(out=path(name, d), defines=[f"{k}={v}" for k, v in d.items()])
         print("built", path(name, d), flush=True)
 
@@ -41,7 +49,8 @@ def build(name):
 def run(name, config):
     for d in SETS[name]:
         env = dict(os.environ, SS_LIB_VARIANT=path(name, d))
-        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--steps", "1000",
+        steps = "1000" if config not in ("2",) else "3000"
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--steps", steps,
                             "--no-e2e", "--no-cpu-baseline"], capture_output=True, text=True, env=env, timeout=300)
         try:
             line = json.loads(r.stdout.strip().splitlines()[-1])
