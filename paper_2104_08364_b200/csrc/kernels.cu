@@ -615,6 +615,9 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 // The grid is split into G interleaved CTA subsets, subset k serving destination region (me + 1 + k) % G: the NVLink
 // stores to every peer and the local-only pass over the own region run at the same time (processing the regions one
 // after another left the own region's HBM pass on the critical path after the NVLink-bound ones).
+#ifndef SS_SCS_U
+#define SS_SCS_U 2          // float4 chunks per thread per iteration (tuning knob)
+#endif
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
   const Ep ep = peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_cons
   const int64_t tid = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
   const int64_t stride = n_cta * blockDim.x;
   const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
-  constexpr int U = 2;
+  constexpr int U = SS_SCS_U;
   const int r = (me + 1 + k) % G;
   const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
   float *dst = a.inbox[r] + slot_off;
@@ -1093,7 +1096,7 @@ cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s) {
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
   const int G = a.sync.world > 0 ? a.sync.world : 1;
-  const int grid = (std::max(grid_for(k, (a.P / 4 + 1) / 2 + 1), G) + G - 1) / G * G;   // every subset has CTAs
+  const int grid = (std::max(grid_for(k, (a.P / 4 + SS_SCS_U - 1) / SS_SCS_U + 1), G) + G - 1) / G * G;  // every subset has CTAs
   k<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
