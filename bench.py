@@ -55,6 +55,25 @@ PROF_NOTE = ("CUDA events around every launch on the library stream, in a second
              "after the uninstrumented timed region")
 
 
+# The JSON line is the only thing bench.py writes to stdout: native libraries (NCCL prints its version banner from
+# the communicator set-up inside the library) write to file descriptor 1 directly, so fd 1 is pointed at stderr for
+# the whole run and the line goes to a private copy of the original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -423,7 +442,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
     g = None
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -467,7 +486,7 @@ def run_scenario(args):
             "scenario": {"switches": [dict(zip(("tick", "version", "to", "reason"), e)) for e in log], **res,
                          "staleness_hist": {str(i): int(x) for i, x in enumerate(st["hist"]) if x}},
             "clocks": clk}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------------------------------
@@ -558,7 +577,7 @@ def run_toy(args):
                          "version": st["version"], "staleness_hist": {str(i): int(x) for i, x in enumerate(st["hist"])
                                                                       if x}},
             "clocks": clk}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------------------------------
@@ -717,7 +736,7 @@ def run_workload(args):
             "speedup_vs_bsp": {k: runs["bsp"]["seconds"] / r["seconds"] for k, r in runs.items()},
             "clocks": clk}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -802,11 +821,12 @@ def run_reference(args):
                              "sample": f"each step on the first {Ps} of {P} elements ({Ps / P:.4f} of the vector), "
                                        f"scaled by P/P_s"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 if __name__ == "__main__":
     a = parse()
+    _claim_stdout()
     if a.impl == "reference":
         run_reference(a)
     elif a.config == "4":
