@@ -618,12 +618,32 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 #ifndef SS_SCS_U
 #define SS_SCS_U 2          // float4 chunks per thread per iteration (tuning knob)
 #endif
+#ifndef SS_SCS_REMOTE_W     // CTAs per remote region : CTAs for the own region, per cycle of the interleave
+#define SS_SCS_REMOTE_W 1   // (tuning knobs; 1 : 1 is an equal split)
+#endif
+#ifndef SS_SCS_LOCAL_W
+#define SS_SCS_LOCAL_W 1
+#endif
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
   const Ep ep = peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
-  const int k = (int)(blockIdx.x % G);
-  const int64_t n_cta = ((int64_t)gridDim.x - k + G - 1) / G;             // CTAs in subset k
-  const int64_t tid = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
+  // interleave cycle of M CTAs: SS_SCS_REMOTE_W per remote region (k = 0 .. G-2), then SS_SCS_LOCAL_W for the own one
+  constexpr int A = SS_SCS_REMOTE_W, B = SS_SCS_LOCAL_W;
+  const int M = (G - 1) * A + B;
+  const int64_t cyc = blockIdx.x / M, full = gridDim.x / M, rem = gridDim.x % M;
+  const int pos = (int)(blockIdx.x % M);
+  int k;
+  int64_t local_cta, n_cta;
+  if (pos < (G - 1) * A) {
+    k = pos / A;
+    local_cta = cyc * A + pos % A;
+    n_cta = full * A + min(max(rem - (int64_t)k * A, (int64_t)0), (int64_t)A);
+  } else {
+    k = G - 1;
+    local_cta = cyc * B + (pos - (G - 1) * A);
+    n_cta = full * B + min(max(rem - (int64_t)(G - 1) * A, (int64_t)0), (int64_t)B);
+  }
+  const int64_t tid = local_cta * blockDim.x + threadIdx.x;
   const int64_t stride = n_cta * blockDim.x;
   const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
   constexpr int U = SS_SCS_U;
@@ -1096,7 +1116,8 @@ cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s) {
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
   const int G = a.sync.world > 0 ? a.sync.world : 1;
-  const int grid = (std::max(grid_for(k, (a.P / 4 + SS_SCS_U - 1) / SS_SCS_U + 1), G) + G - 1) / G * G;  // every subset has CTAs
+  const int M = (G - 1) * SS_SCS_REMOTE_W + SS_SCS_LOCAL_W;                       // whole interleave cycles
+  const int grid = (std::max(grid_for(k, (a.P / 4 + SS_SCS_U - 1) / SS_SCS_U + 1), M) + M - 1) / M * M;
   k<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
