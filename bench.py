@@ -761,6 +761,17 @@ def _oracle_inputs(orc, n, P):
     return w0, gb, ga
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg, seconds: float):
     """The oracle as it stands (single-threaded C), on this host, on a bounded sample: full-size steps until
     `seconds` of CPU work (at least one)."""
@@ -779,7 +790,7 @@ def cpu_baseline(cfg, seconds: float):
             break
     return {"value": k / el, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{k} full-size steps of the same workload ({el:.1f} s, P={P}, n={n})",
-            "host_cpus": os.cpu_count()}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 def run_reference(args):
@@ -817,7 +828,8 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash gradients)",
             "impl": "reference",
             "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
+                             "host_cpus": os.cpu_count(),
                              "sample": f"each step on the first {Ps} of {P} elements ({Ps / P:.4f} of the vector), "
                                        f"scaled by P/P_s"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
