@@ -244,6 +244,25 @@ def run_ours(args):
                 raise ss.SSError(s, g.last_error())
             return ver + 1 + n
 
+        def bsp_only(self, ver):
+            """One BSP superstep (under BSP)."""
+            self.vs[:] = ver
+            s = ss.lib.ss_bsp_step(g.ctx, self.gp_c, self.ws.ctypes.data, self.vs.ctypes.data, self.k)
+            if s:
+                raise ss.SSError(s, g.last_error())
+            return ver + 1
+
+        def asp_window(self, ver, first):
+            """One ASP window under ASP: n pushes, each followed by the pusher's pull. Push j sends the version of
+            its last pull: the switch's version for the first window (a BSP superstep sets every base), afterwards
+            ver - n + j + 1 (staleness n - 1)."""
+            for j in range(n):
+                self.ev[2 * j].version = ver if first else ver - n + j + 1
+            s = ss.lib.ss_asp_replay(g.ctx, self.ev_c, 2 * n, None)
+            if s:
+                raise ss.SSError(s, g.last_error())
+            return ver + n
+
     steps_dev = [Step({(j, r): ring[(j, 2 * q + r)] for j in hosted for r in range(2)}, pull_dst) for q in range(R)]
     n_call = [0]
 
@@ -297,6 +316,36 @@ def run_ours(args):
     total_ms, bsp_ms, asp_ms, prof_ms = t.tolist()
     launches = sum(k["launches"] for k in kst.values())
 
+    # Pure-protocol rates (the metric's "BSP sync steps/s" and "ASP pushes/s" as a training phase runs them):
+    # supersteps back to back, then ASP windows back to back, each run timed by two events on the library's stream
+    # with no per-launch instrumentation (max over ranks).
+    nr = max(20, args.steps // 2)
+    ver = g.version
+    pe = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    barrier()
+    pe[0].record(stream)
+    for t in range(nr):
+        ver = steps_dev[t % R].bsp_only(ver)
+    pe[1].record(stream)
+    barrier()
+    g.switch(ss.SS_ASP, 0)
+    barrier()
+    pe[2].record(stream)
+    for t in range(nr):
+        ver = steps_dev[t % R].asp_window(ver, t == 0)
+    pe[3].record(stream)
+    barrier()
+    g.switch(ss.SS_BSP, 0)
+    pt = torch.tensor([pe[0].elapsed_time(pe[1]), pe[2].elapsed_time(pe[3])], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+    bsp_only_ms, asp_only_ms = pt.tolist()
+    rates = {"bsp_steps_per_s": nr / (bsp_only_ms / 1e3), "bsp_us_per_step": 1e3 * bsp_only_ms / nr,
+             "asp_pushes_per_s": n * nr / (asp_only_ms / 1e3), "asp_us_per_window": 1e3 * asp_only_ms / nr,
+             "supersteps": nr, "windows": nr, "pushes_per_window": n,
+             "note": "pure BSP supersteps back to back, then pure ASP windows (n pushes, each followed by its pull) "
+                     "back to back; two CUDA events per run, no per-launch instrumentation; max over ranks"}
+    ver = g.version
     st = g.stats(64)
     assert st["status"] == 0 and g.sync_status() == 0, g.last_error()
 
@@ -417,6 +466,8 @@ def run_ours(args):
         phases["bsp_nvlink_busbw_GBps"] = per_dir / (bsp_ms / args.steps / 1e3) / 1e9
         phases["bsp_nvlink_frac_of_900"] = phases["bsp_nvlink_busbw_GBps"] / 900.0
         phases["bsp_nvlink_frac_of_770_measured"] = phases["bsp_nvlink_busbw_GBps"] / 770.0
+        rates["bsp_nvlink_busbw_GBps"] = per_dir / (bsp_only_ms / nr / 1e3) / 1e9
+        rates["bsp_nvlink_frac_of_900"] = rates["bsp_nvlink_busbw_GBps"] / 900.0
     line = {
         "metric": METRIC, "value": round(steps_per_s, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -431,7 +482,7 @@ def run_ours(args):
                           f"inputs larger than L2: gradients rotate over {R} sets ({R * set_bytes / 1e6:.0f} MB per "
                           f"rank, >= 3x the 126 MB L2), no flush; PS state w, v ({8 * P / world / 1e6:.1f} MB) and "
                           f"pull buffers stay resident")},
-        "phases": phases, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
+        "phases": phases, "protocol_rates": rates, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
         "graph": graph,
         "e2e": e2e,
         "protocol_check": {"version": st["version"], "hist_0_to_n": [int(x) for x in st["hist"][:n + 1]]},
