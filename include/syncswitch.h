@@ -22,6 +22,10 @@
  *    surfaced no later than the next ss_sync), every later call returns it ("failed training").
  *  - Multi-GPU (one process per GPU): after ss_init_dist, ss_bsp_step, ss_asp_push, ss_pull, ss_asp_replay,
  *    ss_switch, ss_sync and ss_read_params are collective: every rank makes the same call sequence (SPMD).
+ *    Protocol errors (versions, barrier sets, protocol state) are decided on host state every rank shares, so they
+ *    fail on every rank alike. An argument only one rank sees (the hosting rank's gradient or pull destination) can
+ *    fail on that rank alone: the other ranks' fused kernels then give up after 10 s and report SS_E_CUDA at their
+ *    next ss_sync (NCCL mode: the collective blocks) — validate such arguments before the call on every rank.
  */
 #ifndef SYNCSWITCH_H
 #define SYNCSWITCH_H
