@@ -166,7 +166,9 @@ __device__ __forceinline__ bool is_pow2(float d) {
 constexpr int kU1 = SS_BSP_U;  // float4 chunks per thread per iteration
 constexpr int kG1 = SS_BSP_G;  // gradients loaded together
 
-template <bool VEC>
+// U float4 per thread per iteration, GL gradients loaded together (the streaming form uses the sweep's kU1/kG1; a
+// launch smaller than one wave of it uses <1, 4>: profiles/r01_bsp_sweep.txt, config 2)
+template <bool VEC, int U = kU1, int GL = kG1>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
   const Ep ep = peer_enter(a.sync);
   const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
@@ -175,11 +177,11 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
   bool bad = false;
   if (VEC) {
     const int64_t n4 = a.count >> 2;
-    for (int64_t q0 = tid; q0 < n4; q0 += stride * kU1) {
-      float4 acc[kU1], wv[kU1], vv[kU1];
-      bool ok[kU1];
+    for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+      float4 acc[U], wv[U], vv[U];
+      bool ok[U];
 #pragma unroll
-      for (int u = 0; u < kU1; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t q = q0 + u * stride;
         ok[u] = q < n4;
         if (ok[u]) {
@@ -188,21 +190,21 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
           vv[u] = ld4(a.v + 4 * q);
         }
       }
-      for (int j0 = 1; j0 < a.n_in; j0 += kG1) {
-        float4 t[kG1][kU1];
+      for (int j0 = 1; j0 < a.n_in; j0 += GL) {
+        float4 t[GL][U];
 #pragma unroll
-        for (int jj = 0; jj < kG1; ++jj)
+        for (int jj = 0; jj < GL; ++jj)
 #pragma unroll
-          for (int u = 0; u < kU1; ++u)
+          for (int u = 0; u < U; ++u)
             if (j0 + jj < a.n_in && ok[u]) t[jj][u] = ld4(a.g[j0 + jj] + 4 * (q0 + u * stride));
 #pragma unroll
-        for (int jj = 0; jj < kG1; ++jj)
+        for (int jj = 0; jj < GL; ++jj)
 #pragma unroll
-          for (int u = 0; u < kU1; ++u)
+          for (int u = 0; u < U; ++u)
             if (j0 + jj < a.n_in && ok[u]) acc[u] = add4(acc[u], t[jj][u]);  // ascending worker order
       }
 #pragma unroll
-      for (int u = 0; u < kU1; ++u) {
+      for (int u = 0; u < U; ++u) {
         if (!ok[u]) continue;
         up(acc[u].x, wv[u].x, vv[u].x);
         up(acc[u].y, wv[u].y, vv[u].y);
@@ -1040,7 +1042,14 @@ cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
   if (a.count <= 0 && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
   if (vec) {
     auto k = bsp_update_kernel<true>;
-    k<<<grid_for(k, (a.count / 4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
+    const int64_t n4 = a.count / 4;
+    if (n4 < (int64_t)resident_ctas(k) * num_sms() * kThreads * kU1) {
+      // less than one wave of the streaming form (small P, e.g. config 2): latency-bound, one float4 per thread
+      auto ks = bsp_update_kernel<true, 1, 4>;
+      ks<<<grid_for(ks, n4 + 1), kThreads, 0, s>>>(a);
+    } else {
+      k<<<grid_for(k, (n4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
+    }
   } else {
     auto k = bsp_update_kernel<false>;
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
