@@ -1038,8 +1038,23 @@ int grid_for(K kernel, int64_t work_items) {
 
 }  // namespace
 
+#ifndef SS_BSP_CARVEOUT
+#define SS_BSP_CARVEOUT 0   // 1: bsp_update prefers the max shared-memory carveout, the replay kernel's SM configuration
+#endif
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
   if (a.count <= 0 && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
+#if SS_BSP_CARVEOUT
+  static const bool carve = [] {
+    cudaFuncSetAttribute(bsp_update_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(bsp_update_kernel<true, 1, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(bsp_update_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    return true;
+  }();
+  (void)carve;
+#endif
   if (vec) {
     auto k = bsp_update_kernel<true>;
     const int64_t n4 = a.count / 4;
