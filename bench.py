@@ -11,8 +11,9 @@ rotated step by step with R chosen so that R steps' gradients are >= 3x the 126 
 streams ~3.3 GB), so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|2|5a..5d] [--impl ours|reference]
-N > 1: launched by torchrun; one process per GPU, NCCL over NVLink (reduce-scatter / all-gather for BSP,
-owner-routed send/recv for ASP); strong scaling (P and n fixed).
+N > 1: one process per GPU — under torchrun, or started by bench.py itself (torch.distributed.run on 127.0.0.1)
+when WORLD_SIZE is unset; the fused peer-memory exchange over NVLink (scatter -> owner update + broadcast for BSP,
+owner-routed pushes and pulls for ASP), NCCL for set-up and agreement; strong scaling (P and n fixed).
 """
 from __future__ import annotations
 
@@ -173,7 +174,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.config.startswith("5") and world > 1:
+        # n = S = G at G in {2, 4, 8} (one worker and one shard per GPU); n = S = 8 at G = 1
+        cfg.update(n=world, S=world, name=cfg["name"].replace("n=S=8", f"n=S=G={world}"))
     P, n, S, win = cfg["P"], cfg["n"], cfg["S"], args.window or cfg["window"]
     hosted = [j for j in range(n) if (j * world) // n == rank]
 
@@ -887,8 +891,27 @@ def run_reference(args):
     emit(line)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _self_launch(a) -> int:
+    """`--gpus N > 1` from a plain shell (no WORLD_SIZE in the environment): start the N ranks with
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) running this same command line. Rank 0
+    prints the JSON line on the shared stdout; torchrun's own messages go to stderr."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = {**os.environ, "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS", "1")}
+    return subprocess.call(cmd, env=env)
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "ours":
+        sys.exit(_self_launch(a))
     _claim_stdout()
     if a.impl == "reference":
         run_reference(a)

@@ -107,6 +107,8 @@ def lib():
     L.orc_detector_free.argtypes = [_p]
     L.orc_detector_window.restype = _i32
     L.orc_detector_window.argtypes = [_p, _p, _p, _p]
+    L.orc_detector_window_masked.restype = _i32
+    L.orc_detector_window_masked.argtypes = [_p, _p, _p, _p, _p]
     _lib = L
     return L
 
@@ -307,11 +309,16 @@ class Detector:
         self.n = n
         self._h = self._L.orc_detector_new(n, K)
 
-    def window(self, samples, busy):
+    def window(self, samples, busy, mask=None):
+        """One detection window; `mask` (elastic policy): only workers with mask[k] != 0 are measured."""
         s = np.ascontiguousarray(samples, dtype=np.float64)
         b = np.ascontiguousarray(busy, dtype=np.float64)
         flag = np.zeros(self.n, dtype=np.int32)
-        clean = self._L.orc_detector_window(self._h, _ptr(s), _ptr(b), _ptr(flag))
+        if mask is None:
+            clean = self._L.orc_detector_window(self._h, _ptr(s), _ptr(b), _ptr(flag))
+        else:
+            m = np.ascontiguousarray(mask, dtype=np.uint8)
+            clean = self._L.orc_detector_window_masked(self._h, _ptr(s), _ptr(b), _ptr(m), _ptr(flag))
         return flag.astype(bool), bool(clean)
 
     def __del__(self):

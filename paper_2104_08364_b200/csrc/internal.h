@@ -94,41 +94,8 @@ struct ScatterArgs {
   PeerSync sync;
 };
 
-// Pipelined fused BSP: one persistent kernel per rank. Phase-A work items store chunk c of a
-// destination rank's region (this rank's hosted gradient slices, or their pre-sum) into that rank's inbox and raise
-// its per-chunk flag; phase-B items (own region) wait only for their chunk's flags, then reduce, update and broadcast
-// that chunk — the HBM work and both NVLink directions overlap across chunks instead of meeting at a global barrier.
-constexpr int kMaxChunks = 1024;                     // chunks per owner region
-constexpr int kSigChunkBase = 1024;                  // chunk flags start here in the flag block (uint32 index)
-constexpr int kSigWords = kSigChunkBase + kMaxChunks * kMaxPeers;
-
-struct PipeBspArgs {
-  // phase A: sources of this rank, ascending worker id
-  const float *src[kMaxWorkers];
-  int32_t slot[kMaxWorkers];     // exact mode: destination inbox slot of each source (= worker id)
-  int32_t n_src;
-  int32_t presum;                // 1: one slot per rank holds the ascending sum of that rank's sources
-  float *inbox[kMaxPeers];       // every rank's inbox (mapped)
-  uint32_t *flags[kMaxPeers];    // every rank's chunk flags (mapped): [c * kMaxPeers + source rank]
-  int64_t real_lo[kMaxPeers];
-  int64_t cnt[kMaxPeers];        // real elements of each rank's region
-  int64_t chunk_len[kMaxPeers];  // floats per chunk of each rank's region (multiple of 32)
-  int32_t n_chunks[kMaxPeers];
-  int32_t max_chunks;
-  int64_t reg_len;
-  // phase B: this rank's region
-  const float *g[kMaxWorkers];   // terms summed in ascending order, pre-offset to the region start
-  int32_t n_in;
-  float *w, *v;
-  float *bcast[kMaxPeers];
-  int32_t n_bcast;
-  int *flag;
-  float divisor, mu, neg_eta, lam;
-  int32_t nesterov;
-  uint32_t *work;                // item counter (local; the last CTA resets it)
-  uint32_t epoch;                // chunk-flag epoch of this step, as an offset from the device epoch counter
-  PeerSync sync;                 // end barrier: signal + wait
-};
+constexpr int kSigWords = 256;   // flag block (uint32): [0..7] inbound epoch flags, [32] CTA counter, [64] timeout
+                                 // flag, [160] device epoch counter
 
 // What the in-library drivers (scenario.cpp) need to know about a context.
 struct CtxInfo {
@@ -143,7 +110,6 @@ cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s);
 cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s);
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s);
-cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s);
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
                               cudaStream_t s);
 cudaError_t launch_dynamic_criterion(const float *X, const int32_t *y, int32_t B, int32_t d, int32_t C,

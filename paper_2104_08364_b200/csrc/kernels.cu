@@ -308,106 +308,32 @@ __global__ void __launch_bounds__(kThreads) local_sum_kernel(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// K2 asp_replay. Each thread owns kU2 float4 chunks of the slice for the whole window: w and v are read once and
-// written once per window; every push streams its gradient chunk in (prefetched one push ahead), every pull
-// stores the current w chunk — so a pull observes exactly the pushes before it, on every shard (reading C6).
-constexpr int kU2 = 4;
-
-template <bool VEC>
-__global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_constant__ AspArgs a) {
+// K2 asp_replay, scalar form: used only when a gradient or snapshot pointer is not 16-byte aligned (the TMA form
+// below needs 16-byte aligned sources). Same arithmetic, element by element: every push updates w, v in order,
+// every pull stores the current w — so a pull observes exactly the pushes before it, on every shard (reading C6).
+__global__ void __launch_bounds__(kThreads) asp_replay_scalar_kernel(const __grid_constant__ AspArgs a) {
   const Ep ep = peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const float lam = a.lam;
-  bool bad = false;
-  int first_push = 0;
-  while (first_push < a.n_ev && a.ev[first_push].kind != 0) ++first_push;
-
-  // per-push momentum: the post-switch momentum policy may vary it push by push
   const bool nest = a.nesterov != 0;
-  auto apply1 = [&](float g, float &w, float &v, float neg_eta, float mu) {
-    if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
-    v = __fmaf_rn(mu, v, g);
-    w = __fmaf_rn(neg_eta, nest ? __fmaf_rn(mu, v, g) : v, w);
-  };
-
-  if (VEC) {
-    const int64_t n4 = a.count >> 2;
-    for (int64_t q0 = tid; q0 < n4; q0 += stride * kU2) {
-      float4 wv[kU2], vv[kU2], gn[kU2];
-      bool ok[kU2];
-#pragma unroll
-      for (int u = 0; u < kU2; ++u) {
-        const int64_t q = q0 + u * stride;
-        ok[u] = q < n4;
-        if (ok[u]) {
-          wv[u] = ld4(a.w + 4 * q);
-          vv[u] = ld4(a.v + 4 * q);
-          if (first_push < a.n_ev) gn[u] = ld4(a.ev[first_push].src + 4 * q);
-        }
-      }
-      int next = first_push;
-      for (int e = 0; e < a.n_ev; ++e) {
-        const int kind = a.ev[e].kind;
-        if (kind == 0) {
-          float4 gc[kU2];
-#pragma unroll
-          for (int u = 0; u < kU2; ++u) gc[u] = gn[u];
-          next = e + 1;
-          while (next < a.n_ev && a.ev[next].kind != 0) ++next;
-          if (next < a.n_ev) {
-#pragma unroll
-            for (int u = 0; u < kU2; ++u)
-              if (ok[u]) gn[u] = ld4(a.ev[next].src + 4 * (q0 + u * stride));
-          }
-          const float neg_eta = -a.ev[e].lr, mu_e = a.ev[e].mu;
-#pragma unroll
-          for (int u = 0; u < kU2; ++u) {
-            if (!ok[u]) continue;
-            apply1(gc[u].x, wv[u].x, vv[u].x, neg_eta, mu_e);
-            apply1(gc[u].y, wv[u].y, vv[u].y, neg_eta, mu_e);
-            apply1(gc[u].z, wv[u].z, vv[u].z, neg_eta, mu_e);
-            apply1(gc[u].w, wv[u].w, vv[u].w, neg_eta, mu_e);
-          }
-        } else if (a.ev[e].dst != nullptr) {
-          float *dst = a.ev[e].dst;
-#pragma unroll
-          for (int u = 0; u < kU2; ++u)
-            if (ok[u]) st4(dst + 4 * (q0 + u * stride), wv[u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kU2; ++u) {
-        if (!ok[u]) continue;
-        bad |= nonfinite(wv[u].x) | nonfinite(wv[u].y) | nonfinite(wv[u].z) | nonfinite(wv[u].w) |
-               nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
-        const int64_t q = q0 + u * stride;
-        st4(a.w + 4 * q, wv[u]);
-        st4(a.v + 4 * q, vv[u]);
+  bool bad = false;
+  for (int64_t i = tid; i < a.count; i += stride) {
+    float w = a.w[i], v = a.v[i];
+    for (int e = 0; e < a.n_ev; ++e) {
+      if (a.ev[e].kind == 0) {
+        float g = a.ev[e].src[i];
+        if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
+        const float mu = a.ev[e].mu;                  // per-push momentum (post-switch policy)
+        v = __fmaf_rn(mu, v, g);
+        w = __fmaf_rn(-a.ev[e].lr, nest ? __fmaf_rn(mu, v, g) : v, w);
+      } else if (a.ev[e].dst) {
+        a.ev[e].dst[i] = w;
       }
     }
-    const int64_t i = 4 * n4 + tid;
-    if (i < a.count) {
-      float w = a.w[i], v = a.v[i];
-      for (int e = 0; e < a.n_ev; ++e) {
-        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr, a.ev[e].mu);
-        else if (a.ev[e].dst) a.ev[e].dst[i] = w;
-      }
-      bad |= nonfinite(w) | nonfinite(v);
-      a.w[i] = w;
-      a.v[i] = v;
-    }
-  } else {
-    for (int64_t i = tid; i < a.count; i += stride) {
-      float w = a.w[i], v = a.v[i];
-      for (int e = 0; e < a.n_ev; ++e) {
-        if (a.ev[e].kind == 0) apply1(a.ev[e].src[i], w, v, -a.ev[e].lr, a.ev[e].mu);
-        else if (a.ev[e].dst) a.ev[e].dst[i] = w;
-      }
-      bad |= nonfinite(w) | nonfinite(v);
-      a.w[i] = w;
-      a.v[i] = v;
-    }
+    bad |= nonfinite(w) | nonfinite(v);
+    a.w[i] = w;
+    a.v[i] = v;
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
   peer_done(a.sync, ep);
@@ -420,9 +346,6 @@ __global__ void __launch_bounds__(kThreads) asp_replay_kernel(const __grid_const
 // consumers, across push and tile boundaries, so the bytes in flight no longer depend on registers per thread.
 #ifndef SS_TMA_TILE
 #define SS_TMA_TILE 2048   // tuning knobs (tools/kernel_sweep.py builds variants)
-#endif
-#ifndef SS_TMA_BALANCE
-#define SS_TMA_BALANCE 0
 #endif
 #ifndef SS_TMA_STAGES
 #define SS_TMA_STAGES 10   // 80 KB rings -> 2 CTAs per SM: 96.5-98% of the HBM copy vs 93% at 6 stages / 4 CTAs
@@ -617,38 +540,18 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 // The grid is split into G interleaved CTA subsets, subset k serving destination region (me + 1 + k) % G: the NVLink
 // stores to every peer and the local-only pass over the own region run at the same time (processing the regions one
 // after another left the own region's HBM pass on the critical path after the NVLink-bound ones).
-#ifndef SS_SCS_U
-#define SS_SCS_U 2          // float4 chunks per thread per iteration (tuning knob)
-#endif
-#ifndef SS_SCS_REMOTE_W     // CTAs per remote region : CTAs for the own region, per cycle of the interleave
-#define SS_SCS_REMOTE_W 1   // (tuning knobs; 1 : 1 is an equal split)
-#endif
-#ifndef SS_SCS_LOCAL_W
-#define SS_SCS_LOCAL_W 1
-#endif
+constexpr int kScsU = 2;   // float4 chunks per thread per iteration
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
   const Ep ep = peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
-  // interleave cycle of M CTAs: SS_SCS_REMOTE_W per remote region (k = 0 .. G-2), then SS_SCS_LOCAL_W for the own one
-  constexpr int A = SS_SCS_REMOTE_W, B = SS_SCS_LOCAL_W;
-  const int M = (G - 1) * A + B;
-  const int64_t cyc = blockIdx.x / M, full = gridDim.x / M, rem = gridDim.x % M;
-  const int pos = (int)(blockIdx.x % M);
-  int k;
-  int64_t local_cta, n_cta;
-  if (pos < (G - 1) * A) {
-    k = pos / A;
-    local_cta = cyc * A + pos % A;
-    n_cta = full * A + min(max(rem - (int64_t)k * A, (int64_t)0), (int64_t)A);
-  } else {
-    k = G - 1;
-    local_cta = cyc * B + (pos - (G - 1) * A);
-    n_cta = full * B + min(max(rem - (int64_t)(G - 1) * A, (int64_t)0), (int64_t)B);
-  }
+  // interleave cycle of G CTAs: CTA k of each cycle serves region (me + 1 + k) % G (k = G - 1: the own region);
+  // the launcher sizes the grid in whole cycles
+  const int k = (int)(blockIdx.x % G);
+  const int64_t local_cta = blockIdx.x / G, n_cta = gridDim.x / G;
   const int64_t tid = local_cta * blockDim.x + threadIdx.x;
   const int64_t stride = n_cta * blockDim.x;
   const int64_t slot_off = (int64_t)a.slot[0] * a.reg_len;
-  constexpr int U = SS_SCS_U;
+  constexpr int U = kScsU;
   const int r = (me + 1 + k) % G;
   const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
   float *dst = a.inbox[r] + slot_off;
@@ -685,143 +588,6 @@ __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_cons
     dst[i] = acc;
   }
   peer_done(a.sync, ep);
-}
-
-// ---------------------------------------------------------------------------------------------------------------
-// pipe_bsp (fused BSP, pipelined): see PipeBspArgs. The grid is split in two roles. Phase-A CTAs (the first half)
-// claim items (chunk c of rank q's region, c-major so every link carries traffic from the start) from counter 0 and
-// never wait; phase-B CTAs claim chunks of this rank's region from counter 1, in order, and wait only for that
-// chunk's flags — so early chunks are reduced, updated and broadcast while later chunks are still in flight, and no
-// wait can deadlock (every rank's phase A runs to completion). Phase B sums its terms in the fixed ascending order.
-__device__ __forceinline__ void chunk_copy(float *dst, const float *src, int64_t len) {
-  const int64_t n4 = len >> 2;
-  for (int64_t q = threadIdx.x; q < n4; q += 2 * kThreads) {
-    const bool two = q + kThreads < n4;
-    const float4 x0 = ld4(src + 4 * q);
-    float4 x1;
-    if (two) x1 = ld4(src + 4 * (q + kThreads));
-    *reinterpret_cast<float4 *>(dst + 4 * q) = x0;
-    if (two) *reinterpret_cast<float4 *>(dst + 4 * (q + kThreads)) = x1;
-  }
-  for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += kThreads) dst[i] = src[i];
-}
-
-__global__ void __launch_bounds__(kThreads) pipe_bsp_kernel(const __grid_constant__ PipeBspArgs a) {
-  __shared__ uint32_t s_item;
-  const Ep ep = peer_epochs(a.sync);
-  const uint32_t chunk_epoch = ep.signal - a.sync.signal_off + a.epoch;   // base + the chunk-flag offset
-  const int me = a.sync.rank, G = a.sync.world;
-  const uint32_t nA = (uint32_t)(G * a.max_chunks);
-  const uint32_t nB = (uint32_t)a.n_chunks[me];
-  const bool roleA = blockIdx.x < (gridDim.x + 1) / 2;
-  const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
-  bool bad = false;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(a.work + (roleA ? 0 : 1), 1u);
-    __syncthreads();
-    const uint32_t it = roleA ? s_item : nA + s_item;
-    __syncthreads();
-    if (roleA ? it >= nA : it >= nA + nB) break;
-    if (it < nA) {
-      // ---------------- phase A: chunk c of rank q's region ----------------
-      const int c = (int)(it / G), q = (int)(it % G);
-      if (c >= a.n_chunks[q] || (q == me && !a.presum)) continue;
-      const int64_t off = (int64_t)c * a.chunk_len[q];
-      const int64_t len = min(a.chunk_len[q], a.cnt[q] - off);
-      const int64_t gsrc = a.real_lo[q] + off;       // position in the full vector
-      if (a.presum) {
-        float *dst = a.inbox[q] + (int64_t)me * a.reg_len + off;
-        const int64_t n4 = len >> 2;
-        for (int64_t p = threadIdx.x; p < n4; p += kThreads) {
-          float4 acc = a.n_src > 0 ? ld4(a.src[0] + gsrc + 4 * p) : make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int k = 1; k < a.n_src; ++k) acc = add4(acc, ld4(a.src[k] + gsrc + 4 * p));
-          *reinterpret_cast<float4 *>(dst + 4 * p) = acc;
-        }
-        for (int64_t i = 4 * n4 + threadIdx.x; i < len; i += kThreads) {
-          float acc = a.n_src > 0 ? a.src[0][gsrc + i] : 0.0f;
-          for (int k = 1; k < a.n_src; ++k) acc = __fadd_rn(acc, a.src[k][gsrc + i]);
-          dst[i] = acc;
-        }
-      } else {
-        for (int k = 0; k < a.n_src; ++k)
-          chunk_copy(a.inbox[q] + (int64_t)a.slot[k] * a.reg_len + off, a.src[k] + gsrc, len);
-      }
-      __threadfence_system();
-      __syncthreads();
-      if (threadIdx.x == 0) st_release_sys(a.flags[q] + c * kMaxPeers + me, chunk_epoch);
-    } else {
-      // ---------------- phase B: chunk c of this rank's region ----------------
-      const int c = (int)(it - nA);
-      if (threadIdx.x == 0) {
-        const unsigned long long t0 = globaltimer();
-        for (int q = 0; q < G; ++q) {
-          if (q == me && !a.presum) continue;
-          const uint32_t *f = a.flags[me] + c * kMaxPeers + q;
-          while ((int32_t)(ld_acquire_sys(f) - chunk_epoch) < 0) {
-            if (globaltimer() - t0 > kTimeoutNs) {
-              atomicExch(a.sync.err, 1);
-              break;
-            }
-            __nanosleep(64);
-          }
-        }
-      }
-      __syncthreads();
-      const int64_t off = (int64_t)c * a.chunk_len[me];
-      const int64_t len = min(a.chunk_len[me], a.cnt[me] - off);
-      const int64_t n4 = len >> 2;
-      for (int64_t p = threadIdx.x; p < n4; p += kThreads) {
-        const int64_t e = off + 4 * p;
-        float4 acc = ld4(a.g[0] + e);
-        for (int j0 = 1; j0 < a.n_in; j0 += kG1) {
-          float4 t[kG1];
-#pragma unroll
-          for (int jj = 0; jj < kG1; ++jj)
-            if (j0 + jj < a.n_in) t[jj] = ld4(a.g[j0 + jj] + e);
-#pragma unroll
-          for (int jj = 0; jj < kG1; ++jj)
-            if (j0 + jj < a.n_in) acc = add4(acc, t[jj]);     // ascending order
-        }
-        float4 wv = ld4(a.w + e), vv = ld4(a.v + e);
-        up(acc.x, wv.x, vv.x);
-        up(acc.y, wv.y, vv.y);
-        up(acc.z, wv.z, vv.z);
-        up(acc.w, wv.w, vv.w);
-        bad |= nonfinite(wv.x) | nonfinite(wv.y) | nonfinite(wv.z) | nonfinite(wv.w) | nonfinite(vv.x) |
-               nonfinite(vv.y) | nonfinite(vv.z) | nonfinite(vv.w);
-        st4(a.w + e, wv);
-        st4(a.v + e, vv);
-        for (int b = 0; b < a.n_bcast; ++b) *reinterpret_cast<float4 *>(a.bcast[b] + e) = wv;
-      }
-      for (int64_t i = off + 4 * n4 + threadIdx.x; i < off + len; i += kThreads) {
-        float acc = a.g[0][i];
-        for (int j = 1; j < a.n_in; ++j) acc = __fadd_rn(acc, a.g[j][i]);
-        float w = a.w[i], v = a.v[i];
-        up(acc, w, v);
-        bad |= nonfinite(w) | nonfinite(v);
-        a.w[i] = w;
-        a.v[i] = v;
-        for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
-      }
-    }
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *a.flag = 1;
-  // end barrier; the last CTA also rewinds the item counter for the next step
-  __threadfence_system();
-  __syncthreads();
-  __shared__ uint32_t last;
-  if (threadIdx.x == 0) last = atomicAdd(a.sync.ctr, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  if (threadIdx.x == 0) {
-    *a.sync.ctr = 0;
-    a.work[0] = 0;
-    a.work[1] = 0;
-    __threadfence_system();
-    for (int q = 0; q < G; ++q) st_release_sys(a.sync.sig_peer[q] + me, ep.signal);
-    *a.sync.epoch_base = ep.signal;
-  }
-  peer_wait(a.sync, ep.signal);
 }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -1038,23 +804,8 @@ int grid_for(K kernel, int64_t work_items) {
 
 }  // namespace
 
-#ifndef SS_BSP_CARVEOUT
-#define SS_BSP_CARVEOUT 0   // 1: bsp_update prefers the max shared-memory carveout, the replay kernel's SM configuration
-#endif
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
   if (a.count <= 0 && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
-#if SS_BSP_CARVEOUT
-  static const bool carve = [] {
-    cudaFuncSetAttribute(bsp_update_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(bsp_update_kernel<true, 1, 4>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(bsp_update_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    return true;
-  }();
-  (void)carve;
-#endif
   if (vec) {
     auto k = bsp_update_kernel<true>;
     const int64_t n4 = a.count / 4;
@@ -1086,62 +837,41 @@ cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
 
 cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   if ((a.count <= 0 || a.n_ev <= 0) && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
-  static const int variant = [] {  // SS_ASP_KERNEL=reg selects the register-prefetch form (A/B measurement)
-    const char *e = getenv("SS_ASP_KERNEL");
-    return (e && e[0] == 'r') ? 0 : 1;
-  }();
-  if (vec && variant == 1) {
-    static const int r = [] {    // resident CTAs per SM at this kernel's shared memory (thread-safe static init)
-      int res = 0;
-      cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-      cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, asp_replay_tma_kernel<true>, kThreads, kTmaSmem);
-      return res > 0 ? res : 1;
-    }();
-    // Grid-stride over all resident CTAs. Default: fixed kTmaTile tiles. SS_TMA_BALANCE=1 (tuning build): tiles
-    // sized so the range splits into whole waves (whole 128-B lines), leaving no partly idle last wave.
-    const int64_t nvec = (a.count >> 2) << 2;
-    const int64_t slots = (int64_t)r * num_sms();
-    int64_t tile = kTmaTile;
-#if SS_TMA_BALANCE
-    const int64_t waves = std::max<int64_t>(1, (nvec + slots * kTmaTile - 1) / (slots * kTmaTile));
-    tile = std::min<int64_t>(kTmaTile, std::max<int64_t>(256, ((nvec + slots * waves - 1) / (slots * waves) + 31) &
-                                                                    ~(int64_t)31));
-#endif
-    const int64_t tiles = (nvec + tile - 1) / tile;
-    const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
-    AspArgs b = a;
-    b.tile = (int32_t)tile;
-    b.n_push = 0;
-    for (int e = 0; e < a.n_ev; ++e)
-      if (a.ev[e].kind == 0) b.push_ev[b.n_push++] = (uint8_t)e;
-    const int64_t items = (tiles + grid - 1) / grid * b.n_push;   // most gradient tiles any CTA stages
-    if (items > kTmaStages)
-      asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
-    else
-      asp_replay_tma_kernel<false><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
-  } else if (vec) {
-    auto k = asp_replay_kernel<true>;
-    k<<<grid_for(k, (a.count / 4 + kU2 - 1) / kU2 + 1), kThreads, 0, s>>>(a);
-  } else {
-    auto k = asp_replay_kernel<false>;
+  if (!vec) {
+    auto k = asp_replay_scalar_kernel;
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
   }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pipe_bsp(const PipeBspArgs &a, cudaStream_t s) {
-  auto k = pipe_bsp_kernel;
-  const int grid = resident_ctas(k) * num_sms();   // persistent: every CTA resident (items are claimed dynamically)
-  k<<<grid, kThreads, 0, s>>>(a);
+  static const int r = [] {    // resident CTAs per SM at this kernel's shared memory (thread-safe static init)
+    int res = 0;
+    cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, asp_replay_tma_kernel<true>, kThreads, kTmaSmem);
+    return res > 0 ? res : 1;
+  }();
+  // grid-stride over fixed kTmaTile tiles, at most one wave of resident CTAs
+  const int64_t nvec = (a.count >> 2) << 2;
+  const int64_t slots = (int64_t)r * num_sms();
+  const int64_t tile = kTmaTile;
+  const int64_t tiles = (nvec + tile - 1) / tile;
+  const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
+  AspArgs b = a;
+  b.tile = (int32_t)tile;
+  b.n_push = 0;
+  for (int e = 0; e < a.n_ev; ++e)
+    if (a.ev[e].kind == 0) b.push_ev[b.n_push++] = (uint8_t)e;
+  const int64_t items = (tiles + grid - 1) / grid * b.n_push;   // most gradient tiles any CTA stages
+  if (items > kTmaStages)
+    asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
+  else
+    asp_replay_tma_kernel<false><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
   const int G = a.sync.world > 0 ? a.sync.world : 1;
-  const int M = (G - 1) * SS_SCS_REMOTE_W + SS_SCS_LOCAL_W;                       // whole interleave cycles
-  const int grid = (std::max(grid_for(k, (a.P / 4 + SS_SCS_U - 1) / SS_SCS_U + 1), M) + M - 1) / M * M;
+  const int grid = (std::max(grid_for(k, (a.P / 4 + kScsU - 1) / kScsU + 1), G) + G - 1) / G * G;   // whole cycles
   k<<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -80,6 +80,7 @@ struct ss_ctx {
   float *w = nullptr;                  // replica [P_pad]; authoritative on the owned region
   float *v = nullptr;                  // momentum of the owned region [reg_len]
   int *flag = nullptr;                 // non-finite flag
+  int *health = nullptr;               // G > 1: [flag, barrier timeout] agreed over ranks at ss_sync
   float *sum_buf = nullptr;            // G > 1: local pre-sum [P_pad]
   float *rs_buf = nullptr;             // G > 1: reduce-scattered sum [reg_len]
   std::vector<float *> stage;          // full-length staging slots for host pointers (a ring, see stage_slot)
@@ -105,6 +106,7 @@ struct ss_ctx {
   std::vector<int64_t> log;            // 4 per applied gradient
   // window batcher
   std::vector<Ev> win;
+  std::vector<int32_t> win_kind, win_worker;   // mirror of win for the cut rule
   int32_t max_win = 16;
   // fused peer-memory path (G > 1): CUDA-IPC-mapped inboxes, replicas, pull buffers and flags
   int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed
@@ -112,7 +114,7 @@ struct ss_ctx {
   int64_t inbox_slots = 0;
   float *inbox = nullptr;              // [inbox_slots][reg_len] gradient slices owned here, written by peers
   float *pbuf = nullptr;               // [n_hosted][P_pad] pull buffers of hosted workers, written by owners
-  uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag, [96..] pipe work, [160] epoch counter
+  uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag, [160] epoch counter
   float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
   uint32_t *peer_sig[ss::kMaxPeers] = {};
   std::vector<void *> opened;          // peer mappings to close
@@ -156,12 +158,16 @@ ss_status fail(ss_ctx *c, ss_status s, const char *fmt, ...) {
   return s;
 }
 
+// On failure the runtime's last-error slot is cleared (cudaGetLastError): a recoverable error (an allocation that
+// failed) must not resurface as the launch status of a later kernel.
 #define SS_CUDA(c, call)                                                                                 \
   do {                                                                                                   \
     cudaError_t e_ = (call);                                                                             \
-    if (e_ != cudaSuccess)                                                                               \
+    if (e_ != cudaSuccess) {                                                                             \
+      cudaGetLastError();                                                                                \
       return fail((c), e_ == cudaErrorMemoryAllocation ? SS_E_OOM : SS_E_CUDA, "%s: %s (%s:%d)", #call, \
                   cudaGetErrorString(e_), __FILE__, __LINE__);                                           \
+    }                                                                                                    \
   } while (0)
 
 #define SS_NCCL(c, call)                                                                                        \
@@ -631,6 +637,8 @@ ss_status flush_fused(ss_ctx *c) {
     if (e.host_dst) SS_TRY(pull_to_host(c, e));
   }
   c->win.clear();
+  c->win_kind.clear();
+  c->win_worker.clear();
   return SS_OK;
 }
 
@@ -702,7 +710,6 @@ ss_status flush(ss_ctx *c) {
       a.count = cnt;
       a.lam = c->lam;
       a.nesterov = c->nesterov;
-  a.nesterov = c->nesterov;
       Timed t;
       timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
       SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
@@ -727,6 +734,8 @@ ss_status flush(ss_ctx *c) {
   for (const Ev &e : c->win)
     if (e.kind == 1 && e.host_dst) SS_TRY(pull_to_host(c, e));
   c->win.clear();
+  c->win_kind.clear();
+  c->win_worker.clear();
   return SS_OK;
 }
 
@@ -753,16 +762,15 @@ ss_status check_live(ss_ctx *c) {
   return SS_OK;
 }
 
-// Appends an event to the pending window (flushing first when the window must be cut). The event's host staging —
-// the H2D of a host gradient, the slot of a host pull destination — is set up after that cut, so a window's slots
-// all belong to it.
-ss_status enqueue(ss_ctx *c, Ev e, const float *src = nullptr, float *pull_dst = nullptr) {
-  std::vector<int32_t> kd, wk;
-  for (const Ev &x : c->win) {
-    kd.push_back(x.kind);
-    wk.push_back(x.worker);
-  }
-  if (ss::window_cut(kd.data(), wk.data(), (int32_t)kd.size(), e.kind, e.worker, c->max_win,
+// Appending an event to the pending window is split so that a call either applies completely or not at all (SV §8b
+// "errors never partially apply"): enqueue_prepare does everything that can fail — the capture check for host
+// buffers, the window cut (device work of earlier, already accepted calls), the staging of host data — before the
+// caller touches any protocol state; enqueue_commit cannot fail. The event's staging follows the cut, so a window's
+// slots all belong to it. win_kind / win_worker mirror the window for the cut rule (no per-call rebuild).
+ss_status enqueue_prepare(ss_ctx *c, Ev &e, const float *src, float *pull_dst) {
+  if (c->capturing && ((src && is_host_ptr(src)) || (pull_dst && is_host_ptr(pull_dst))))
+    return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
+  if (ss::window_cut(c->win_kind.data(), c->win_worker.data(), (int32_t)c->win.size(), e.kind, e.worker, c->max_win,
                      c->world > 1 && c->fused_mode != 0))
     SS_TRY(flush(c));
   if (e.kind == 0 && src) SS_TRY(resolve_src(c, src, &e.src));
@@ -776,8 +784,35 @@ ss_status enqueue(ss_ctx *c, Ev e, const float *src = nullptr, float *pull_dst =
       e.dst = pull_dst;
     }
   }
+  return SS_OK;
+}
+
+void enqueue_commit(ss_ctx *c, const Ev &e) {
   c->win.push_back(e);
-  if ((int32_t)c->win.size() >= c->max_win) return flush(c);
+  c->win_kind.push_back(e.kind);
+  c->win_worker.push_back(e.worker);
+}
+
+// A full window is launched right away (eagerly: its device work then overlaps the host's next calls).
+ss_status flush_if_full(ss_ctx *c) { return (int32_t)c->win.size() >= c->max_win ? flush(c) : SS_OK; }
+
+// Multi-GPU: each rank's kernels see only its own owned slice, so a non-finite value or a timed-out cross-GPU
+// barrier is first known to one rank. ss_sync is collective: the ranks agree on both words (NCCL max) before
+// deciding, so every rank becomes DIVERGED (or reports the timeout) at the same ss_sync.
+ss_status agree_health(ss_ctx *c, int *div, int *timeout) {
+  if (c->world == 1 || !c->comm) return SS_OK;
+  if (!c->health) SS_CUDA(c, cudaMalloc(&c->health, 2 * sizeof(int)));
+  SS_CUDA(c, cudaMemcpyAsync(c->health, c->flag, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+  if (c->ipc_ready)
+    SS_CUDA(c, cudaMemcpyAsync(c->health + 1, c->sigblk + 64, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+  else
+    SS_CUDA(c, cudaMemsetAsync(c->health + 1, 0, sizeof(int), c->stream));
+  SS_NCCL(c, ncclAllReduce(c->health, c->health, 2, ncclInt32, ncclMax, c->comm, c->stream));
+  int h[2] = {0, 0};
+  SS_CUDA(c, cudaMemcpyAsync(h, c->health, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  SS_CUDA(c, cudaStreamSynchronize(c->stream));
+  *div = h[0];
+  *timeout = h[1];
   return SS_OK;
 }
 
@@ -786,14 +821,14 @@ ss_status sync_impl(ss_ctx *c) {
   SS_CUDA(c, cudaStreamSynchronize(c->stream));
   if (c->copy_in) SS_CUDA(c, cudaStreamSynchronize(c->copy_in));
   if (c->copy_out) SS_CUDA(c, cudaStreamSynchronize(c->copy_out));
-  int h = 0;
-  SS_CUDA(c, cudaMemcpy(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
-  if (h) c->diverged = true;
-  if (c->ipc_ready) {
-    int t = 0;
-    SS_CUDA(c, cudaMemcpy(&t, c->sigblk + 64, sizeof(int), cudaMemcpyDeviceToHost));
-    if (t) return fail(c, SS_E_CUDA, "fused path: a cross-GPU barrier timed out (a peer did not arrive)");
+  int h = 0, t = 0;
+  if (c->world > 1 && c->comm) {
+    SS_TRY(agree_health(c, &h, &t));
+  } else {
+    SS_CUDA(c, cudaMemcpy(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
   }
+  if (h) c->diverged = true;
+  if (t) return fail(c, SS_E_CUDA, "fused path: a cross-GPU barrier timed out (a peer did not arrive)");
   if (c->diverged) return fail(c, SS_E_DIVERGED, "diverged: a non-finite parameter or momentum was produced");
   return SS_OK;
 }
@@ -901,7 +936,7 @@ void ss_destroy(ss_ctx *c) {
             cudaSuccess) {
       const std::string path = c->trace_path + ".rank" + std::to_string(c->rank) + ".csv";
       if (FILE *f = fopen(path.c_str(), "w")) {
-        static const char *names[] = {"scatter", "scatter_sum", "bsp_update", "asp_replay", "pipe_bsp"};
+        static const char *names[] = {"scatter", "scatter_sum", "bsp_update", "asp_replay"};
         fprintf(f, "launch,kernel,enter_ns,waited_ns,signal_ns,end_ns\n");
         for (size_t i = 0; i < c->trace_kind.size(); ++i)
           fprintf(f, "%zu,%s,%llu,%llu,%llu,%llu\n", i, names[c->trace_kind[i]], h[4 * i], h[4 * i + 1],
@@ -937,6 +972,7 @@ void ss_destroy(ss_ctx *c) {
   cudaFree(c->w);
   cudaFree(c->v);
   cudaFree(c->flag);
+  cudaFree(c->health);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -999,15 +1035,6 @@ ss_status ss_current_lr(ss_ctx *c, int32_t proto, float *lr_out) {
   return SS_OK;
 }
 
-// The pipelined fused BSP kernel (pipe_bsp) is kept for experiments; the two-kernel form measured faster so far.
-bool bsp_pipe_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("SS_BSP_PIPE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *workers, const int64_t *versions,
                       int32_t n_local) {
   SS_TRY(check_live(c));
@@ -1036,6 +1063,9 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     for (int32_t i = 0; i < n_local; ++i)
       if (!aligned16(grads[i]) && !is_host_ptr(grads[i]))
         return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
+  if (c->capturing)
+    for (int32_t i = 0; i < n_local; ++i)
+      if (is_host_ptr(grads[i])) return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
   SS_TRY(flush(c));
   c->stepped = true;
 
@@ -1067,64 +1097,6 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     Timed t;
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
-    timed_end(c, &t);
-  } else if (c->fused_mode != 0 && bsp_pipe_enabled() && !c->nvls.ready) {
-    // Fused peer-memory BSP, pipelined (experimental, SS_BSP_PIPE=1; kernels.cu pipe_bsp): one persistent kernel per rank.
-    // Phase-A items store chunk slices of this rank's hosted gradients (mode 1) or of their ascending pre-sum (mode 2)
-    // into the owners' inboxes and raise per-chunk flags; phase-B items reduce, update and broadcast each chunk of the
-    // owned region as soon as its flags are up. One end barrier closes the step.
-    const bool presum = c->fused_mode == 2;
-    SS_TRY(ensure_fused(c, presum ? c->world : c->n));
-    const uint32_t epA = ++c->epoch, epB = ++c->epoch;
-    const int32_t me = c->rank;
-    const int64_t lo = c->real_lo[me];
-    ss::PipeBspArgs pa;
-    std::memset(&pa, 0, sizeof pa);
-    pa.n_src = k;
-    for (int32_t i = 0; i < k; ++i) {
-      if (!aligned16(a.g[i])) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
-      pa.src[i] = a.g[i];
-      pa.slot[i] = ids[i];
-    }
-    pa.presum = presum ? 1 : 0;
-    pa.reg_len = c->reg_len;
-    for (int32_t q = 0; q < c->world; ++q) {
-      pa.inbox[q] = c->peer_inbox[q];
-      pa.flags[q] = c->peer_sig[q] + ss::kSigChunkBase;
-      pa.real_lo[q] = c->real_lo[q];
-      pa.cnt[q] = c->real_hi[q] - c->real_lo[q];
-      int64_t nch = pa.cnt[q] > 0 ? std::min<int64_t>(ss::kMaxChunks, (pa.cnt[q] + 65535) / 65536) : 0;
-      pa.chunk_len[q] = nch > 0 ? ((pa.cnt[q] + nch - 1) / nch + 31) / 32 * 32 : 32;
-      pa.n_chunks[q] = nch > 0 ? (int32_t)((pa.cnt[q] + pa.chunk_len[q] - 1) / pa.chunk_len[q]) : 0;
-      pa.max_chunks = std::max(pa.max_chunks, pa.n_chunks[q]);
-    }
-    int32_t ni = 0, h = 0;
-    if (presum) {
-      for (int32_t q = 0; q < c->world; ++q) pa.g[ni++] = c->inbox + (int64_t)q * c->reg_len;
-    } else {
-      for (int32_t j = 0; j < c->n; ++j) {   // the members' slices, ascending worker order
-        if (!c->member[j]) continue;
-        pa.g[ni++] = host_of(c, j) == me ? a.g[h++] + lo : c->inbox + (int64_t)j * c->reg_len;
-      }
-    }
-    pa.n_in = ni;
-    pa.w = c->w + lo;
-    pa.v = c->v;
-    for (int32_t q = 0; q < c->world; ++q)
-      if (q != me) pa.bcast[pa.n_bcast++] = c->peer_w[q] + lo;
-    pa.flag = c->flag;
-    pa.divisor = a.divisor;
-    pa.mu = a.mu;
-    pa.neg_eta = a.neg_eta;
-    pa.lam = a.lam;
-    pa.nesterov = a.nesterov;
-    pa.work = c->sigblk + 96;
-    pa.epoch = epA - c->dev_epoch;   // chunk-flag epoch as an offset from the device counter (see peer_sync)
-    pa.sync = peer_sync(c, 0, epB, true, 4);
-    Timed t;
-    const double cnt_me = (double)(c->real_hi[me] - lo);
-    timed_begin(c, &t, 0, 4.0 * cnt_me * (ni + 4));
-    SS_CUDA(c, ss::launch_pipe_bsp(pa, c->stream));
     timed_end(c, &t);
   } else if (c->fused_mode != 0) {
     // Fused peer-memory BSP. Phase A: scatter hosted gradients (exact mode) or this rank's
@@ -1248,14 +1220,16 @@ ss_status ss_asp_push(ss_ctx *c, int32_t worker, const float *grad, int64_t vers
   Ev e{};
   e.kind = 0;
   e.worker = worker;
-  e.lr = lr_at(c, c->version, SS_ASP);
+  e.lr = lr_at(c, c->version, SS_ASP);   // pre-increment version (reading C9)
   e.mu = asp_momentum(c, c->version);
+  SS_TRY(enqueue_prepare(c, e, mine ? grad : nullptr, nullptr));   // may fail: nothing of this push applied yet
+  enqueue_commit(c, e);
   const int64_t st = c->version - version;
   record(c, worker, version, st);
   c->version += 1;
   c->stepped = true;
   if (staleness_out) *staleness_out = st;
-  return enqueue(c, e, mine ? grad : nullptr);
+  return flush_if_full(c);
 }
 
 ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
@@ -1266,14 +1240,17 @@ ss_status ss_pull(ss_ctx *c, int32_t worker, float *dst, int64_t *version_out) {
   // and send their owned slices).
   if (c->world > 1 && mine && !dst) return fail(c, SS_E_INVAL, "multi-GPU pull needs a destination");
   SS_TRY(maybe_switch(c));
-  c->base[worker] = c->version;
-  if (version_out) *version_out = c->version;
   Ev e{};
   e.kind = 1;
   e.worker = worker;
   e.data = c->world > 1 || dst != nullptr;
-  if (!e.data) return SS_OK;
-  return enqueue(c, e, nullptr, mine ? dst : nullptr);
+  if (e.data) {
+    SS_TRY(enqueue_prepare(c, e, nullptr, mine ? dst : nullptr));   // may fail: the base version is not moved yet
+    enqueue_commit(c, e);
+  }
+  c->base[worker] = c->version;
+  if (version_out) *version_out = c->version;
+  return e.data ? flush_if_full(c) : SS_OK;
 }
 
 ss_status ss_switch(ss_ctx *c, int32_t proto, int64_t at_step) {

@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--host-buffers", type=int, default=0, help="gradients and pull destinations in host memory")
     ap.add_argument("--scenario", type=int, default=-1, help="run ss_scenario_run with this policy instead")
     ap.add_argument("--nesterov", type=int, default=0)
+    ap.add_argument("--nan-bsp", type=int, default=0,
+                    help="after --bsp1 supersteps, one superstep whose worker-0 gradient is NaN at the last element "
+                         "(owned by the last rank); every rank records its ss_sync status")
     ap.add_argument("--capture", type=int, default=-1,
                     help="bench step (BSP + switch + n push/pull + switch) once, captured once, replayed this often")
     a = ap.parse_args()
@@ -131,6 +134,19 @@ def main():
     for _ in range(a.bsp1):
         gs = {j: grad(j) for j in range(n)}
         g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
+    if a.nan_bsp:
+        gs = {j: grad(j) for j in range(n)}
+        if 0 in hosted:
+            gs[0][P - 1] = float("nan")
+            torch.cuda.synchronize()
+        s1 = g.bsp_step_status([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
+        s2 = g.sync_status()                 # collective: every rank must see the divergence here
+        s3 = g.bsp_step_status([gs[j] for j in hosted], hosted, [g.version] * len(hosted))   # sticky
+        np.savez(os.path.join(a.out, f"rank{rank}.npz"), status=np.array([s1, s2, s3]), hosted=np.array(hosted))
+        g.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if a.drop >= 0:
         members = [j for j in range(n) if j != a.drop]
         g.set_members(members)

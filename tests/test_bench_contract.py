@@ -34,3 +34,26 @@ def test_gpu_line_recorded_with_required_keys():
     assert set(rf) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+def test_multi_gpu_self_launch_command(monkeypatch):
+    """`python bench.py --gpus N` from a plain shell starts its own N ranks (torch.distributed.run, 127.0.0.1); under
+    torchrun (WORLD_SIZE set) it runs as the rank it is."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+
+    def fake_call(cmd, env=None):
+        seen["cmd"], seen["env"] = cmd, env
+        return 0
+
+    monkeypatch.setattr(bench.subprocess, "call", fake_call)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "20", "--warmup", "5"])
+    a = bench.parse()
+    assert bench._self_launch(a) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-6:] == ["--gpus", "4", "--steps", "20", "--warmup", "5"]
+    assert cmd[-7].endswith("bench.py")

@@ -154,7 +154,7 @@ def close_c13(x, y, rel=1e-5):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case_seed", list(range(4)))
+@pytest.mark.parametrize("case_seed", list(range(8)))
 def test_random_protocol_sequences_multi_gpu(orc, world, case_seed):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")

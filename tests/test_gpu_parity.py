@@ -404,6 +404,10 @@ def test_softmax_grad_kernel(ss, orc):
     loss = torch.empty(1, device="cuda")
     assert ss.ss_softmax_grad(Xd, yd, B, d, C, Wd, grad, loss) == 0
     lo, go = orc.softmax_loss_grad(X[:B], y[:B], W.astype(np.float64))
+    # elementwise within the a-priori fp32 bound of the kernel's operation order (tests/criterion_bounds.py)
+    from criterion_bounds import softmax_grad_bounds
+    Eg = softmax_grad_bounds(X[:B], y[:B], W.astype(np.float64))["Eg"]
+    assert np.all(np.abs(grad.cpu().numpy() - go) <= Eg + 1e-12 * np.abs(go))
     assert close_c13(grad.cpu().numpy(), go) and abs(loss.item() - lo) <= 1e-5 * abs(lo)
     # zero parameters: loss = ln C exactly up to fp32 rounding
     assert ss.ss_softmax_grad(Xd, yd, B, d, C, torch.zeros(d * C, device="cuda"), grad, loss) == 0

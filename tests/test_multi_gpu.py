@@ -99,7 +99,9 @@ def test_multi_gpu_parity(orc, world, case):
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop, bsp_drop, nesterov=nest)
     exact = case in ("asp_only", "switched_fused", "elastic_fused", "nesterov_fused")   # NCCL / pre-summed: other sum orders (C13)
     ow, ov = o.params(), o.velocity()
-    for r in res:
+    for q, r in enumerate(res):
+        # worker placement: the oracle's worker -> GPU map (a1)
+        assert [int(j) for j in r["hosted"]] == [j for j in range(n) if orc.worker_host(j, n, world) == q]
         # protocol integers: exact on every rank
         assert list(r["stale"]) == stale
         assert np.array_equal(r["log"], o.log())
@@ -125,11 +127,12 @@ def test_multi_gpu_parity(orc, world, case):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fused", [1, 2])
-def test_multi_gpu_full_size_sampled(orc, world, fused):
+@pytest.mark.parametrize("fused,nvls", [(1, 0), (2, 0), (1, 1), (2, 1)])
+def test_multi_gpu_full_size_sampled(orc, world, fused, nvls):
     """Config 3 at full size (P = 25,557,032, n = S = 8, window 16: the bench's configuration) on `world` GPUs:
     1 BSP superstep, a switch, 16 seeded ASP pushes with pulls, a switch back and 1 BSP superstep; 4,096 sampled
-    elements against the oracle (bit-exact in fused-exact mode, C13 in pre-summed mode), integers exact."""
+    elements against the oracle (bit-exact in fused-exact mode, C13 in pre-summed mode), integers exact. nvls = 1
+    forces the NVSwitch-multicast broadcast (SS_NVLS=1), the default branch from 8 GPUs on."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -137,8 +140,10 @@ def test_multi_gpu_full_size_sampled(orc, world, fused):
     P, n, S = 25_557_032, 8, 8
     with tempfile.TemporaryDirectory() as tmp:
         launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 16, "--bsp1", 1, "--pushes", 16,
-                       "--bsp2", 1, "--fused", fused, "--sample", 4096], tmp)
+                       "--bsp2", 1, "--fused", fused, "--sample", 4096], tmp, env={"SS_NVLS": str(nvls)})
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    if nvls and not all(int(r["nvls"]) for r in res):
+        pytest.skip("NVLS multicast unavailable on this box")
     idx = sample_indices(P, 4096)
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 1, 16, 1, idx=idx)
     exact = fused == 1
@@ -309,3 +314,28 @@ def test_multi_gpu_scenario(orc, world, policy):
         assert list(r["res"]) == [out[k] for k in ("bsp_steps", "asp_pushes", "dropped", "end_tick", "version")]
         assert np.array_equal(r["plog"], o.log()) and np.array_equal(r["hist"], o.stats(64)["hist"])
         assert np.array_equal(r["w"], o.params()) and np.array_equal(r["v"], o.velocity())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [0, 1, 2])
+def test_multi_gpu_divergence_reaches_every_rank(orc, world, fused):
+    """A non-finite gradient element owned by the last rank: only that rank's kernels see the non-finite update, but
+    ss_sync is collective and agrees on the divergence flag, so EVERY rank returns SS_E_DIVERGED at the same ss_sync
+    and stays diverged (sticky). The oracle diverges on the same superstep."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S = 4099, 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--bsp1", 2, "--fused", fused, "--nan-bsp", 1], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    for k in range(2):
+        assert o.bsp_step([orc.synth_grad(SEED, j, k, 0, P) for j in range(n)]) == 0
+    gs = [orc.synth_grad(SEED, j, 2, 0, P) for j in range(n)]
+    gs[0][P - 1] = np.nan
+    first = o.bsp_step(gs)
+    assert first in (0, 6) and o.bsp_step(gs) == 6            # the oracle diverges on this superstep (sticky)
+    for r in res:
+        s1, s2, s3 = (int(x) for x in r["status"])
+        assert s1 in (0, 6) and s2 == 6 and s3 == 6, (s1, s2, s3)

@@ -66,6 +66,28 @@ def test_shard_layout(orc, P, S, pad, ppad):
             assert owners == sorted(owners) and collections.Counter(owners) == {g: S // G for g in range(G)}
 
 
+def test_worker_host_hand_cases(orc):
+    # P:1071 (one PS per worker node) and SURVEY §8(a) a1: worker j runs on GPU floor(j*G/n) -- hand-enumerated cases
+    cases = {
+        (8, 1): [0] * 8,
+        (8, 2): [0, 0, 0, 0, 1, 1, 1, 1],
+        (8, 4): [0, 0, 1, 1, 2, 2, 3, 3],
+        (8, 8): [0, 1, 2, 3, 4, 5, 6, 7],          # the paper's one worker per node
+        (3, 2): [0, 0, 1],                         # floor(0)=0, floor(2/3)=0, floor(4/3)=1
+        (2, 4): [0, 2],                            # more GPUs than workers: GPUs 1 and 3 host nobody
+        (5, 3): [0, 0, 1, 1, 2],                   # floor(0, .6, 1.2, 1.8, 2.4)
+    }
+    for (n, G), want in cases.items():
+        assert [orc.worker_host(j, n, G) for j in range(n)] == want, (n, G)
+    # every GPU hosts floor(n/G) or ceil(n/G) workers, in contiguous ascending blocks, when n >= G
+    for n in range(1, 40):
+        for G in (1, 2, 3, 4, 8):
+            h = [orc.worker_host(j, n, G) for j in range(n)]
+            assert h == sorted(h) and all(0 <= x < G for x in h)
+            if n >= G:
+                assert set(collections.Counter(h).values()) <= {n // G, -(-n // G)}
+
+
 # ---------------------------------------------------------------------------------------------------------------
 # the paper's worked ASP example and BSP on the same gradients
 def _asp_rows():
@@ -333,25 +355,39 @@ def test_switch_fraction_endpoints(orc):
     P, n = 300, 4
     w0 = rng.standard_normal(P).astype(np.float32)
     gs = [[rng.standard_normal(P).astype(np.float32) * 0.01 for _ in range(n)] for _ in range(6)]
-    # s = 1 (switch never reached) == pure BSP
-    a = orc.Oracle(w0, 3, n, 0.1, 0.9)
-    b = orc.Oracle(w0, 3, n, 0.1, 0.9)
+    # s = 1 (the switch point is never reached within the run) == pure BSP == momentum SGD on the mean of the n
+    # gradients at lr n*eta, against a plain numpy fp64 loop
+    b = orc.Oracle(w0.astype(np.float64), 3, n, 0.1, 0.9, dtype=np.float64)
     b.switch(ASP, 6)
+    lr_bsp = float(np.float32(float(np.float32(0.1)) * n))
+    mu = float(np.float32(0.9))
+    w, v = w0.astype(np.float64), np.zeros(P)
     for r in range(6):
-        assert a.bsp_step(gs[r]) == 0 and b.bsp_step(gs[r]) == 0
-    assert np.array_equal(a.params(), b.params())
-    # s = 0 == pure ASP
-    c = orc.Oracle(w0, 3, n, 0.1, 0.9)
+        assert b.bsp_step([x.astype(np.float64) for x in gs[r]]) == 0
+        v = mu * v + np.mean([x.astype(np.float64) for x in gs[r]], axis=0)
+        w = w - lr_bsp * v
+    assert b.version == 6 and b.stats()["protocol"] == ASP     # the switch takes effect only once version reaches 6
+    np.testing.assert_allclose(b.params(), w, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(b.velocity(), v, rtol=1e-13, atol=1e-15)
+    # s = 0 == pure ASP from the first update: with every push preceded by its worker's pull (staleness 0), pure
+    # ASP is sequential momentum SGD at the ASP lr eta/sqrt(n). Checked against a plain numpy
+    # loop in fp64 (the oracle's fp64 instantiation; numpy's separate multiply and add differ from the oracle's FMA
+    # by a few fp64 ulps only).
+    c = orc.Oracle(w0.astype(np.float64), 3, n, 0.1, 0.9, dtype=np.float64)
     c.switch(ASP, 0)
-    d = orc.Oracle(w0, 3, n, 0.1, 0.9)
-    d.switch(ASP, -5)
+    # lr and mu cross the C-ABI as fp32 (reading C12): lr = fp32(fp32(0.1)/sqrt(n)), mu = fp32(0.9)
+    lr_asp = float(np.float32(float(np.float32(0.1)) / math.sqrt(n)))
+    w, v = w0.astype(np.float64), np.zeros(P)
     for r in range(6):
         for j in range(n):
             ver = c.pull(j, False)[2]
-            assert c.asp_push(j, gs[r][j], ver)[0] == 0
-            ver = d.pull(j, False)[2]
-            assert d.asp_push(j, gs[r][j], ver)[0] == 0
-    assert np.array_equal(c.params(), d.params())
+            rc, st = c.asp_push(j, gs[r][j].astype(np.float64), ver)
+            assert rc == 0 and st == 0
+            v = mu * v + gs[r][j].astype(np.float64)
+            w = w - lr_asp * v
+    assert c.version == 6 * n
+    np.testing.assert_allclose(c.velocity(), v, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(c.params(), w, rtol=1e-13, atol=1e-15)
 
 
 def test_switch_preserves_state_and_drops_inflight(orc):
@@ -492,6 +528,38 @@ def test_detector_arithmetic(orc):
     assert dt2.window([100, 100, 100, 60], [1, 1, 1, 1])[0][3]
     # throughput is samples / busy time: 4x the busy time for the same samples is a 4x slower worker
     assert list(dt2.window([10, 10, 10, 10], [1, 1, 1, 4])[0]) == [False, False, False, True]
+
+
+def test_detector_masked_arithmetic(orc):
+    # Elastic policy (reading C25): only the workers still at the BSP barrier are measured. Hand arithmetic:
+    # unmasked (100, 100, 100, 60, 0): S = 72, sigma_pop = sqrt((3*28^2 + 12^2 + 72^2)/5) = sqrt(1536) = 39.19,
+    # threshold 32.81 -> only worker 4 is below; with worker 4 masked out the statistics are those of
+    # (100, 100, 100, 60): S = 90, sigma = 17.32, threshold 72.68 -> worker 3 is below.
+    thr, ones = [100.0, 100.0, 100.0, 60.0, 0.0], [1.0] * 5
+    mask = [1, 1, 1, 1, 0]
+    assert math.sqrt((3 * 28 ** 2 + 12 ** 2 + 72 ** 2) / 5) == pytest.approx(39.1918, rel=1e-5)
+    dt = orc.Detector(5, 3)
+    for _ in range(2):                                   # worker 4 below the threshold twice (run = 2, not yet 3)
+        f, clean = dt.window(thr, ones)
+        assert not f.any() and not clean
+    f, _ = dt.window(thr, ones, mask)                    # masked: worker 4 not measured -> its run restarts at 0
+    assert not f.any()
+    f, _ = dt.window(thr, ones, mask)
+    assert not f.any()                                   # worker 3: 2 consecutive windows, not yet K = 3
+    f, clean = dt.window(thr, ones, mask)
+    assert list(f) == [False, False, False, True, False] and not clean   # worker 3 flagged after 3; worker 4 never
+    f, _ = dt.window(thr, ones)                          # unmasked again: worker 4 starts from 1, not 3 (reset),
+    assert not f.any()                                   # and worker 3 (60 > 32.81) is no longer below
+    f, _ = dt.window(thr, ones)
+    assert not f.any()
+    f, _ = dt.window(thr, ones)
+    assert list(f) == [False, False, False, False, True]
+    # a masked-out worker's throughput does not enter S or sigma: masking the slow worker with any value leaves the
+    # others' statistics (100, 100, 100, 100) -> sigma = 0, nobody flagged
+    dt1 = orc.Detector(5, 1)
+    for junk in (0.0, 1e9, 55.0):
+        f, _ = dt1.window([100.0] * 4 + [junk], ones, [1, 1, 1, 1, 0])
+        assert not f.any()
 
 
 # ---------------------------------------------------------------------------------------------------------------

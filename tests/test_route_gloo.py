@@ -1,4 +1,4 @@
-"""Multi-rank host logic of the N > 1 path on CPU: world-size 2 and 4 processes over torch.distributed 'gloo'.
+"""Multi-rank host logic of the N > 1 path on CPU: world-size 2, 4 and 8 processes over torch.distributed 'gloo'.
 
 Each rank computes its own routing plan with the library's ss_route_plan (the plan.h code the runtime executes with
 NCCL or fused NVLink stores), the ranks cross-check that every send has its matching receive, then EXECUTE the plan
@@ -121,7 +121,7 @@ def _rank_main(rank, world, port, cfg, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("fused", [0, 1])
 @pytest.mark.parametrize("P", [1003, 33])
 def test_route_plan_gloo(world, fused, P):
