@@ -556,12 +556,12 @@ def run_toy(args):
     import numpy as np
     import torch
 
-    from inputs import minibatch_order, toy_dataset
+    from inputs import TOY_RECIPE, minibatch_order, toy_split
     from paper_2104_08364_b200 import syncswitch as ss
     cfg = CONFIGS["1"]
     n, S, B, d, C = cfg["n"], cfg["S"], 16, 1024, 8
     P = d * C
-    X, y = toy_dataset(seed=1)                 # the SURVEY §8(d) recipe (separable classes, eta 0.1, mu 0.9)
+    X, y, Xte, yte = toy_split()               # overlapping classes: still training at the switch (eta 0.1, mu 0.9)
     s_, (bsp_steps, asp_pushes, _) = ss.ss_table1(100 * B, B, n, 1, 2, [])
     ss.ss_check(s_)
     order = minibatch_order(1, len(X), n * bsp_steps + asp_pushes, B)
@@ -606,8 +606,9 @@ def run_toy(args):
         g.sync()
         ms = e0.elapsed_time(e1)
         st_ = g.stats(64)
+        w_end = g.params()
         g.close()
-        return ms, st_
+        return ms, st_, w_end
 
     for _ in range(max(args.warmup, 1)):
         one_run()
@@ -618,7 +619,12 @@ def run_toy(args):
     ms = sum(r[0] for r in runs)
     updates = (bsp_steps + asp_pushes) * args.steps
     lv = losses.cpu().numpy()
-    st = runs[-1][1]
+    st, w_end = runs[-1][1], runs[-1][2]
+    # held-out evaluation of the final parameters (reporting only; not part of the timed path)
+    Wm = w_end.reshape(d, C).astype(np.float64)
+    test_acc = float(np.mean(np.argmax(Xte @ Wm, 1) == yte))
+    train_acc = float(np.mean(np.argmax(X @ Wm, 1) == y))
+    k_sw = n * bsp_steps                       # losses of the BSP phase come first (n per superstep)
     line = {"metric": METRIC, "value": round(updates / (ms / 1e3), 1),
             "unit": "protocol updates/s (BSP supersteps + ASP pushes, each with its softmax_grad kernel(s))",
             "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": ms / args.steps,
@@ -627,7 +633,11 @@ def run_toy(args):
             "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "batch": B,
                        "bsp_steps": bsp_steps, "asp_pushes": asp_pushes, "asp_window_events": 1,
                        "note": "a step = one whole training run from w = 0"},
-            "training": {"loss_first": float(lv[0]), "loss_last10_mean": float(lv[-10:].mean()),
+            "training": {"loss_first": float(lv[0]), "loss_first10_mean": float(lv[:10].mean()),
+                         "loss_at_switch_last10_bsp_mean": float(lv[k_sw - 10:k_sw].mean()),
+                         "loss_last10_mean": float(lv[-10:].mean()),
+                         "test_accuracy": test_acc, "train_accuracy": train_acc,
+                         "data_recipe": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in TOY_RECIPE.items()},
                          "loss_every_10th_update": [round(float(x), 5) for x in lv[::10]],
                          "version": st["version"], "staleness_hist": {str(i): int(x) for i, x in enumerate(st["hist"])
                                                                       if x}},

@@ -37,6 +37,25 @@ def test_lr_at_paper_values(orc):
         assert lr == pytest.approx(want, rel=1e-6), step
 
 
+def test_lr_schedule_in_the_state_machine(orc):
+    # P:1600 step decay applied by the protocol state: the factor is looked up at the PRE-increment version (reading
+    # C9) and is right-continuous at a boundary. n = 1, mu = 0, unit gradients, w0 = 0: w_k = -sum of the lrs used.
+    o = orc.Oracle([0.0], 1, 1, 0.1, 0.0, dtype=np.float64)
+    assert o.set_lr_schedule([2, 4], [0.5, 0.25]) == 0
+    eta = float(np.float32(0.1))
+    lrs = [float(np.float32(eta * f)) for f in (1, 1, 0.5, 0.5, 0.25)]
+    w = 0.0
+    for k in range(5):
+        assert o.current_lr(BSP) == pytest.approx(lrs[k], rel=1e-7)
+        assert o.bsp_step([[1.0]]) == 0
+        w -= lrs[k]
+        assert o.params()[0] == pytest.approx(w, rel=1e-12), k
+    # the same schedule under ASP (eta/sqrt(n) = eta at n = 1), continuing the version count
+    o.switch(ASP, 0)
+    assert o.asp_push(0, [1.0], o.version) == (0, 0)
+    assert o.params()[0] == pytest.approx(w - lrs[4], rel=1e-12)
+
+
 def test_config_policy_values(orc):
     # BSP lr = n*eta (linear scaling); ASP lr = eta/sqrt(n); n = 8, eta = 0.1
     assert orc.lr(0.1, 1.0, BSP, 8) == np.float32(0.8)
