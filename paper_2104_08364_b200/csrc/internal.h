@@ -59,24 +59,33 @@ struct SumArgs {
   int32_t n_in;
 };
 
-// asp_replay (SV §2.5 K2): a window of pushes and pulls applied in arrival order to one owner slice.
+// asp_replay (SV §2.5 K2): a window of events applied in order to one owner slice — ASP pushes and pulls
+// and, on one GPU, BSP supersteps (the ascending sum of the barrier workers'
+// gradients, the mean, the momentum update). Every event is elementwise, so one pass over the slice applies the whole
+// window tile by tile with w and v held on chip: bit-identical to applying the events one after another.
+constexpr int kMaxBspSrc = 128;                    // BSP gradients per window (all BSP events together)
+constexpr int kMaxItems = kMaxEvents + kMaxBspSrc; // gradient tiles staged per tile of the slice
 struct AspEvent {
   const float *src;   // push: gradient slice
   float *dst;         // pull: snapshot destination slice (nullptr: no data)
-  float lr;           // push: eta_ASP at the push's version
-  float mu;           // push: momentum for this push (constant unless a post-switch momentum policy is set)
-  int32_t kind;       // 0 push, 1 pull
+  float lr;           // push / BSP: eta at the event's (pre-increment) version
+  float mu;           // push / BSP: momentum for this update (push: the post-switch momentum policy)
+  float divisor;      // BSP: number of barrier workers (the mean is sum / divisor)
+  int32_t kind;       // 0 push, 1 pull, 2 BSP superstep
+  int32_t src0;       // BSP: its gradients are bsp_src[src0 .. src0 + n_src), ascending worker order
+  int32_t n_src;
 };
 struct AspArgs {
   AspEvent ev[kMaxEvents];
+  const float *bsp_src[kMaxBspSrc];
   float *w;
   float *v;
   int *flag;
   int64_t count;
   int32_t n_ev;
   int32_t tile;       // TMA form: floats per tile (multiple of 32, <= kTmaTile); set by launch_asp_replay
-  int32_t n_push;     // TMA form: number of push events and their indices in window order (set by the launcher)
-  uint8_t push_ev[kMaxEvents];
+  int32_t n_item;     // TMA form: gradient sources per tile, in event order (set by the launcher)
+  const float *item[kMaxItems];
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;

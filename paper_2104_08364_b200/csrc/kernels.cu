@@ -309,8 +309,8 @@ __global__ void __launch_bounds__(kThreads) local_sum_kernel(const __grid_consta
 
 // ---------------------------------------------------------------------------------------------------------------
 // K2 asp_replay, scalar form: used only when a gradient or snapshot pointer is not 16-byte aligned (the TMA form
-// below needs 16-byte aligned sources). Same arithmetic, element by element: every push updates w, v in order,
-// every pull stores the current w — so a pull observes exactly the pushes before it, on every shard (reading C6).
+// below needs 16-byte aligned sources). Same arithmetic, element by element: every event updates w, v in window order
+// and every pull stores the current w — so a pull observes exactly the updates before it, on every shard (C6).
 __global__ void __launch_bounds__(kThreads) asp_replay_scalar_kernel(const __grid_constant__ AspArgs a) {
   const Ep ep = peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -321,14 +321,19 @@ __global__ void __launch_bounds__(kThreads) asp_replay_scalar_kernel(const __gri
   for (int64_t i = tid; i < a.count; i += stride) {
     float w = a.w[i], v = a.v[i];
     for (int e = 0; e < a.n_ev; ++e) {
-      if (a.ev[e].kind == 0) {
-        float g = a.ev[e].src[i];
+      const AspEvent &x = a.ev[e];
+      if (x.kind == 0) {
+        float g = x.src[i];
         if (lam != 0.0f) g = __fmaf_rn(lam, w, g);   // g + f(w) at the PS's current w
-        const float mu = a.ev[e].mu;                  // per-push momentum (post-switch policy)
-        v = __fmaf_rn(mu, v, g);
-        w = __fmaf_rn(-a.ev[e].lr, nest ? __fmaf_rn(mu, v, g) : v, w);
-      } else if (a.ev[e].dst) {
-        a.ev[e].dst[i] = w;
+        v = __fmaf_rn(x.mu, v, g);                    // per-push momentum (post-switch policy)
+        w = __fmaf_rn(-x.lr, nest ? __fmaf_rn(x.mu, v, g) : v, w);
+      } else if (x.kind == 2) {
+        float acc = a.bsp_src[x.src0][i];
+        for (int k = 1; k < x.n_src; ++k) acc = __fadd_rn(acc, a.bsp_src[x.src0 + k][i]);   // ascending workers
+        const Upd up{x.divisor, 1.0f / x.divisor, x.mu, -x.lr, lam, is_pow2(x.divisor), nest};
+        up(acc, w, v);
+      } else if (x.dst) {
+        x.dst[i] = w;
       }
     }
     bad |= nonfinite(w) | nonfinite(v);
@@ -382,17 +387,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-// kRefill = false: every CTA's items (tiles x pushes) fit the ring, so no stage is ever reused and the per-push CTA
-// barrier is dropped (small P; a separate instantiation because a runtime-conditional barrier costs the large-P
-// loop 2.5%: profiles/r01_replay_condsync.txt).
+// kRefill = false: every CTA's items (tiles x gradient sources) fit the ring, so no stage is ever reused and the
+// per-item CTA barrier is dropped (small P; a separate instantiation because a runtime-conditional barrier costs the
+// large-P loop 2.5%: profiles/r01_replay_condsync.txt).
+// Window events: push (one staged gradient tile), BSP superstep (n_src staged tiles summed in ascending worker order
+// into a register accumulator, then the mean and the momentum update), pull (store of the current w).
 template <bool kRefill>
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
   const Ep ep = peer_enter(a.sync);
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
-  __shared__ int push_ev[kMaxEvents];
+  __shared__ const float *item_src[kMaxItems];
   const float lam = a.lam;
-  if (threadIdx.x < a.n_push) push_ev[threadIdx.x] = a.push_ev[threadIdx.x];
+  const bool nest = a.nesterov != 0;
+  for (int k = threadIdx.x; k < a.n_item; k += blockDim.x) item_src[k] = a.item[k];
   if (threadIdx.x == 0) {
     // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
     // (generic proxy): order them after the acquire
@@ -401,23 +409,36 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int n_push = a.n_push;                               // push events in window order (a.push_ev)
+  const int n_item = a.n_item;                               // gradient sources per tile, in event order
   const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
   const int64_t tsz = a.tile;                                // floats per tile (<= kTmaTile)
   const int64_t n_tiles = (nvec + tsz - 1) / tsz;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t items = my_tiles * n_push;                   // one gradient tile per (tile, push)
+  const int64_t items = my_tiles * n_item;                   // one gradient tile per (tile, source)
 
   auto issue = [&](int64_t it) {                             // thread 0: stage the gradient tile of item `it`
-    const int64_t tile = blockIdx.x + (it / n_push) * gridDim.x;
+    const int64_t tile = blockIdx.x + (it / n_item) * gridDim.x;
     const int64_t off = tile * tsz;
     const int64_t len = min(tsz, nvec - off);
     const int s = (int)(it % kTmaStages);
     mbar_expect_tx(&full[s], (uint32_t)(len * 4));
-    bulk_g2s(ring + s * kTmaTile, a.ev[push_ev[it % n_push]].src + off, (uint32_t)(len * 4), &full[s]);
+    bulk_g2s(ring + s * kTmaTile, item_src[it % n_item] + off, (uint32_t)(len * 4), &full[s]);
   };
   if (threadIdx.x == 0)
     for (int64_t it = 0; it < items && it < kTmaStages; ++it) issue(it);
+  // wait for item `it` and hand back its stage: returns the thread's float4 u of the staged tile
+  auto staged = [&](int64_t it, int u) -> float4 {
+    return *reinterpret_cast<const float4 *>(ring + (int)(it % kTmaStages) * kTmaTile + 4 * (threadIdx.x + u * kThreads));
+  };
+  auto release = [&](int64_t it) {
+    if (kRefill) {                                          // (a window that fits the ring never reuses a stage)
+      __syncthreads();                                      // every thread is done with the stage of item `it`
+      if (threadIdx.x == 0 && it + kTmaStages < items) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(it + kTmaStages);
+      }
+    }
+  };
 
   bool bad = false;
   int64_t it = 0;
@@ -436,31 +457,49 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
       }
     }
     for (int e = 0; e < a.n_ev; ++e) {
-      if (a.ev[e].kind == 0) {
-        const int s = (int)(it % kTmaStages);
-        mbar_wait(&full[s], (uint32_t)((it / kTmaStages) & 1));
+      const int kind = a.ev[e].kind;
+      if (kind == 0) {
+        mbar_wait(&full[(int)(it % kTmaStages)], (uint32_t)((it / kTmaStages) & 1));
         const float neg_eta = -a.ev[e].lr, mu = a.ev[e].mu;
 #pragma unroll
         for (int u = 0; u < kTU; ++u) {
           if (!ok[u]) continue;
-          float4 g = *reinterpret_cast<const float4 *>(ring + s * kTmaTile + 4 * (threadIdx.x + u * kThreads));
+          float4 g = staged(it, u);
           float *gp = &g.x, *wp = &wv[u].x, *vp = &vv[u].x;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             float gg = gp[c];
             if (lam != 0.0f) gg = __fmaf_rn(lam, wp[c], gg);   // g + f(w) at the PS's current w
             vp[c] = __fmaf_rn(mu, vp[c], gg);
-            wp[c] = __fmaf_rn(neg_eta, a.nesterov ? __fmaf_rn(mu, vp[c], gg) : vp[c], wp[c]);
+            wp[c] = __fmaf_rn(neg_eta, nest ? __fmaf_rn(mu, vp[c], gg) : vp[c], wp[c]);
           }
         }
-        if (kRefill) {                                          // (a window that fits the ring never reuses a
-          __syncthreads();                                      // stage) every thread is done with stage s
-          if (threadIdx.x == 0 && it + kTmaStages < items) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(it + kTmaStages);
-          }
-        }
+        release(it);
         ++it;
+      } else if (kind == 2) {
+        float4 acc[kTU];
+        const int ns = a.ev[e].n_src;
+        for (int k = 0; k < ns; ++k) {
+          mbar_wait(&full[(int)(it % kTmaStages)], (uint32_t)((it / kTmaStages) & 1));
+#pragma unroll
+          for (int u = 0; u < kTU; ++u) {
+            if (!ok[u]) continue;
+            const float4 g = staged(it, u);
+            acc[u] = k == 0 ? g : add4(acc[u], g);            // ascending worker order (reading C12)
+          }
+          release(it);
+          ++it;
+        }
+        const float dv = a.ev[e].divisor;
+        const Upd up{dv, 1.0f / dv, a.ev[e].mu, -a.ev[e].lr, lam, is_pow2(dv), nest};
+#pragma unroll
+        for (int u = 0; u < kTU; ++u) {
+          if (!ok[u]) continue;
+          up(acc[u].x, wv[u].x, vv[u].x);
+          up(acc[u].y, wv[u].y, vv[u].y);
+          up(acc[u].z, wv[u].z, vv[u].z);
+          up(acc[u].w, wv[u].w, vv[u].w);
+        }
       } else if (a.ev[e].dst != nullptr) {
 #pragma unroll
         for (int u = 0; u < kTU; ++u)
@@ -483,13 +522,19 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     if (i < a.count) {
       float w = a.w[i], v = a.v[i];
       for (int e = 0; e < a.n_ev; ++e) {
-        if (a.ev[e].kind == 0) {
-          float gg = a.ev[e].src[i];
+        const AspEvent &x = a.ev[e];
+        if (x.kind == 0) {
+          float gg = x.src[i];
           if (lam != 0.0f) gg = __fmaf_rn(lam, w, gg);
-          v = __fmaf_rn(a.ev[e].mu, v, gg);
-          w = __fmaf_rn(-a.ev[e].lr, a.nesterov ? __fmaf_rn(a.ev[e].mu, v, gg) : v, w);
-        } else if (a.ev[e].dst) {
-          a.ev[e].dst[i] = w;
+          v = __fmaf_rn(x.mu, v, gg);
+          w = __fmaf_rn(-x.lr, nest ? __fmaf_rn(x.mu, v, gg) : v, w);
+        } else if (x.kind == 2) {
+          float acc = a.bsp_src[x.src0][i];
+          for (int k = 1; k < x.n_src; ++k) acc = __fadd_rn(acc, a.bsp_src[x.src0 + k][i]);
+          const Upd up{x.divisor, 1.0f / x.divisor, x.mu, -x.lr, lam, is_pow2(x.divisor), nest};
+          up(acc, w, v);
+        } else if (x.dst) {
+          x.dst[i] = w;
         }
       }
       bad |= nonfinite(w) | nonfinite(v);
@@ -857,10 +902,13 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
   AspArgs b = a;
   b.tile = (int32_t)tile;
-  b.n_push = 0;
-  for (int e = 0; e < a.n_ev; ++e)
-    if (a.ev[e].kind == 0) b.push_ev[b.n_push++] = (uint8_t)e;
-  const int64_t items = (tiles + grid - 1) / grid * b.n_push;   // most gradient tiles any CTA stages
+  b.n_item = 0;                  // the gradient sources of one tile, in event order
+  for (int e = 0; e < a.n_ev; ++e) {
+    if (a.ev[e].kind == 0) b.item[b.n_item++] = a.ev[e].src;
+    else if (a.ev[e].kind == 2)
+      for (int k = 0; k < a.ev[e].n_src; ++k) b.item[b.n_item++] = a.bsp_src[a.ev[e].src0 + k];
+  }
+  const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
   if (items > kTmaStages)
     asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
   else

@@ -27,7 +27,7 @@ namespace {
 constexpr int kMaxSchedule = 64;
 
 struct Ev {
-  int32_t kind;         // 0 push, 1 pull
+  int32_t kind;         // 0 push, 1 pull, 2 BSP superstep (one GPU: BSP supersteps join the window, see ss_bsp_step)
   int32_t worker;
   const float *src;     // push: device gradient (full length; staged if the caller's was host memory);
                         //       nullptr on ranks not hosting the worker
@@ -35,8 +35,10 @@ struct Ev {
   float *host_dst;      // pull into host memory: D2H from dst after the window
   int32_t slot = -1;    // staging slot behind dst (host destination), or -1
   float lr;             // push: eta_ASP at the push's (pre-increment) version
-  float mu;             // push: momentum (post-switch momentum policy)
+  float mu;             // push: momentum (post-switch momentum policy); BSP: momentum
   bool data;            // pull: moves parameters (false: version-only pull, G = 1)
+  float divisor = 1.f;  // BSP: number of barrier workers
+  int32_t src0 = 0, n_src = 0;   // BSP: gradients win_bsp_src[src0 .. src0 + n_src), ascending workers
 };
 
 struct KStat {
@@ -106,7 +108,8 @@ struct ss_ctx {
   std::vector<int64_t> log;            // 4 per applied gradient
   // window batcher
   std::vector<Ev> win;
-  std::vector<int32_t> win_kind, win_worker;   // mirror of win for the cut rule
+  std::vector<int32_t> win_kind, win_worker;   // the window's ASP events (push / pull) for the cut rule
+  std::vector<const float *> win_bsp_src;      // gradients of the window's BSP events
   int32_t max_win = 16;
   // fused peer-memory path (G > 1): CUDA-IPC-mapped inboxes, replicas, pull buffers and flags
   int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed
@@ -140,7 +143,7 @@ struct ss_ctx {
   bool prof = false;
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> event_pool;
-  KStat kstat[4];
+  KStat kstat[5];                      // 0 bsp_update, 1 asp_replay, 2 local_sum, 3 scatter, 4 window with BSP events
   std::string err;
 };
 
@@ -639,6 +642,7 @@ ss_status flush_fused(ss_ctx *c) {
   c->win.clear();
   c->win_kind.clear();
   c->win_worker.clear();
+  c->win_bsp_src.clear();
   return SS_OK;
 }
 
@@ -647,9 +651,10 @@ ss_status flush(ss_ctx *c) {
   if (c->world > 1 && c->fused_mode != 0) return flush_fused(c);
   const int32_t me = c->rank;
   const int64_t lo = c->real_lo[me], hi = c->real_hi[me], cnt = hi - lo;
-  int32_t n_push = 0, n_pull = 0;
+  int32_t n_push = 0, n_pull = 0, n_bsp_src = 0;
   for (const Ev &e : c->win) {
     if (e.kind == 0) ++n_push;
+    else if (e.kind == 2) n_bsp_src += e.n_src;
     else if (e.data) ++n_pull;
   }
 
@@ -677,7 +682,7 @@ ss_status flush(ss_ctx *c) {
   }
 
   if (cnt > 0) {
-    if (n_push == 0 && c->world == 1) {
+    if (n_push == 0 && n_bsp_src == 0 && c->world == 1) {
       // pulls only: plain copies of the current w
       for (const Ev &e : c->win)
         if (e.data) SS_CUDA(c, cudaMemcpyAsync(e.dst, c->w, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -696,12 +701,22 @@ ss_status flush(ss_ctx *c) {
           x.lr = e.lr;
           x.mu = e.mu;
           vec = vec && aligned16(x.src);
+        } else if (e.kind == 2) {   // one GPU only: the superstep's gradients in ascending worker order
+          x.lr = e.lr;
+          x.mu = e.mu;
+          x.divisor = e.divisor;
+          x.src0 = e.src0;
+          x.n_src = e.n_src;
         } else {
           if (!e.data) continue;  // version-only pull: no data
           x.dst = (c->world == 1 || host_of(c, e.worker) == me) ? e.dst + lo : c->sslot[k];
           vec = vec && aligned16(x.dst);
         }
         ++ne;
+      }
+      for (size_t k = 0; k < c->win_bsp_src.size(); ++k) {
+        a.bsp_src[k] = c->win_bsp_src[k];
+        vec = vec && aligned16(a.bsp_src[k]);
       }
       a.n_ev = ne;
       a.w = c->w + lo;
@@ -711,7 +726,7 @@ ss_status flush(ss_ctx *c) {
       a.lam = c->lam;
       a.nesterov = c->nesterov;
       Timed t;
-      timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull));
+      timed_begin(c, &t, n_bsp_src ? 4 : 1, 4.0 * (double)cnt * (4 + n_push + n_pull + n_bsp_src));
       SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
       timed_end(c, &t);
     }
@@ -736,6 +751,7 @@ ss_status flush(ss_ctx *c) {
   c->win.clear();
   c->win_kind.clear();
   c->win_worker.clear();
+  c->win_bsp_src.clear();
   return SS_OK;
 }
 
@@ -745,7 +761,9 @@ ss_status maybe_switch(ss_ctx *c) {
   if (c->has_pending && c->version >= c->pending_at) {
     c->has_pending = false;
     if (c->pending_proto != c->proto) {
-      SS_TRY(flush(c));
+      // one GPU: every queued event carries its own lr / momentum, so the window may span the switch; at G > 1 BSP
+      // runs outside the windows (exchange kernels), so the ASP window is applied first
+      if (c->world > 1) SS_TRY(flush(c));
       c->proto = c->pending_proto;
       if (c->proto == SS_BSP)
         for (auto &b : c->base) b = c->version;
@@ -770,8 +788,9 @@ ss_status check_live(ss_ctx *c) {
 ss_status enqueue_prepare(ss_ctx *c, Ev &e, const float *src, float *pull_dst) {
   if (c->capturing && ((src && is_host_ptr(src)) || (pull_dst && is_host_ptr(pull_dst))))
     return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
-  if (ss::window_cut(c->win_kind.data(), c->win_worker.data(), (int32_t)c->win.size(), e.kind, e.worker, c->max_win,
-                     c->world > 1 && c->fused_mode != 0))
+  if (ss::window_cut(c->win_kind.data(), c->win_worker.data(), (int32_t)c->win_kind.size(), e.kind, e.worker,
+                     c->max_win, c->world > 1 && c->fused_mode != 0) ||
+      (int32_t)c->win.size() >= ss::kMaxEvents)
     SS_TRY(flush(c));
   if (e.kind == 0 && src) SS_TRY(resolve_src(c, src, &e.src));
   if (e.kind == 1 && pull_dst) {
@@ -789,12 +808,14 @@ ss_status enqueue_prepare(ss_ctx *c, Ev &e, const float *src, float *pull_dst) {
 
 void enqueue_commit(ss_ctx *c, const Ev &e) {
   c->win.push_back(e);
+  if (e.kind == 2) return;
   c->win_kind.push_back(e.kind);
   c->win_worker.push_back(e.worker);
 }
 
-// A full window is launched right away (eagerly: its device work then overlaps the host's next calls).
-ss_status flush_if_full(ss_ctx *c) { return (int32_t)c->win.size() >= c->max_win ? flush(c) : SS_OK; }
+// A window holding max_win ASP events is launched right away (eagerly: its device work then overlaps the host's next
+// calls).
+ss_status flush_if_full(ss_ctx *c) { return (int32_t)c->win_kind.size() >= c->max_win ? flush(c) : SS_OK; }
 
 // Multi-GPU: each rank's kernels see only its own owned slice, so a non-finite value or a timed-out cross-GPU
 // barrier is first known to one rank. ss_sync is collective: the ranks agree on both words (NCCL max) before
@@ -1066,6 +1087,39 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   if (c->capturing)
     for (int32_t i = 0; i < n_local; ++i)
       if (is_host_ptr(grads[i])) return fail(c, SS_E_STATE, "host buffers cannot be used while capturing a graph");
+  if (c->world == 1 && n_local <= ss::kMaxBspSrc) {
+    // One GPU: the superstep joins the pending window as a BSP event (the window kernel sums its gradients in
+    // ascending worker order and applies the mean and the momentum update tile by tile, with w and v on chip, before
+    // the window's later pushes and pulls: bit-identical to a separate update, without the w, v round trip through
+    // HBM). Room first: the window's gradient list, its event array and the staging ring must take the superstep.
+    int32_t host_grads = 0;
+    for (int32_t i = 0; i < n_local; ++i) host_grads += is_host_ptr(grads[i]) ? 1 : 0;
+    if ((int64_t)c->win_bsp_src.size() + n_local > ss::kMaxBspSrc || (int32_t)c->win.size() >= ss::kMaxEvents ||
+        (host_grads && (int64_t)c->win_slots.size() + host_grads > stage_cap(c)))
+      SS_TRY(flush(c));
+    Ev e{};
+    e.kind = 2;
+    e.lr = lr_at(c, c->version, SS_BSP);     // pre-increment version (reading C9)
+    e.mu = c->mu;
+    e.divisor = (float)c->n_members;
+    e.src0 = (int32_t)c->win_bsp_src.size();
+    std::vector<const float *> src;
+    for (int32_t j = 0; j < c->n; ++j) {     // ascending worker order (reading C12)
+      if (!by[j]) continue;
+      const float *g = nullptr;
+      SS_TRY(resolve_src(c, by[j], &g));       // may fail: nothing of this superstep is applied yet
+      src.push_back(g);
+    }
+    e.n_src = (int32_t)src.size();
+    c->win_bsp_src.insert(c->win_bsp_src.end(), src.begin(), src.end());
+    enqueue_commit(c, e);
+    c->stepped = true;
+    for (int32_t j = 0; j < c->n; ++j)
+      if (c->member[j]) record(c, j, c->version, 0);  // one staleness-0 record per BSP member
+    c->version += 1;
+    for (auto &b : c->base) b = c->version;
+    return SS_OK;
+  }
   SS_TRY(flush(c));
   c->stepped = true;
 
@@ -1483,7 +1537,7 @@ ss_status ss_profile(ss_ctx *c, int32_t on) {
 
 ss_status ss_kernel_stats(ss_ctx *c, int32_t id, int64_t *launches, double *ms, double *bytes,
                           double *nvlink_bytes) {
-  if (!c || id < 0 || id > 3) return SS_E_INVAL;
+  if (!c || id < 0 || id > 4) return SS_E_INVAL;
   SS_TRY(drain_timed(c));
   if (launches) *launches = c->kstat[id].launches;
   if (ms) *ms = c->kstat[id].ms;

@@ -659,3 +659,69 @@ def test_max_workers_bsp(ss, orc):
     assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
     assert g.stats(2)["hist"][0] == 2 * n
     g.close()
+
+
+# ---------------------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", ["device", "unaligned", "host"])
+@pytest.mark.parametrize("P,n,S,window", [(100003, 8, 8, 16), (4099, 3, 2, 5), (2 ** 20 + 3, 8, 8, 64)])
+def test_windows_with_bsp_supersteps(ss, orc, mode, P, n, S, window):
+    """One GPU: BSP supersteps join the pending window (one kernel applies supersteps, pushes and pulls tile by tile,
+    w and v on chip). A long program without sync points — 20 supersteps (crossing the window's 128-gradient cap at
+    n = 8), a switch, a seeded ASP phase with pulls, a switch back, more supersteps, an lr boundary inside — is
+    bit-identical to the oracle for device, unaligned (scalar kernel) and host (staged) gradients."""
+    w0 = init_params(orc, P)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    g.set_window(window)
+    for x in (g, o):
+        x.set_lr_schedule([17, 40], [0.5, 0.25])
+    k = {j: 0 for j in range(n)}
+    keep = []
+
+    def grad(j):
+        kk = k[j]
+        k[j] += 1
+        h = host_synth(orc, j, kk, P)
+        if mode == "host":
+            d = torch.from_numpy(h).pin_memory() if kk % 2 else h          # pinned and pageable
+        else:
+            d = dev_synth(ss, j, kk, P, offset=1 if mode == "unaligned" else 0)
+        keep.append(d)
+        return d, h
+
+    def bsp_round():
+        gs = [grad(j) for j in range(n)]
+        v = o.version
+        g.bsp_step([x[0] for x in gs], list(range(n)), [v] * n)
+        assert o.bsp_step([x[1] for x in gs]) == 0
+
+    for _ in range(20):
+        bsp_round()
+    g.switch(ASP, 0)
+    o.switch(ASP, 0)
+    kind, worker, _ = orc.schedule(n, [1000 + 50 * j for j in range(n)], 30, jitter=100, seed=7)
+    base_g, base_o, snaps = {}, {}, []
+    for kd, j in zip(kind, worker):
+        j = int(j)
+        if kd == 1:
+            dst = torch.empty(P, device="cuda") if mode != "host" else np.zeros(P, np.float32)
+            base_g[j] = g.pull(j, dst)
+            _, s_o, base_o[j] = o.pull(j)
+            snaps.append((dst, s_o))
+        else:
+            d, h = grad(j)
+            sg = g.asp_push(j, d, base_g[j])
+            rc, so = o.asp_push(j, h, base_o[j])
+            assert rc == 0 and sg == so
+    g.switch(BSP, 0)
+    o.switch(BSP, 0)
+    for _ in range(5):
+        bsp_round()
+    g.sync()
+    assert g.version == o.version == 25 + 30
+    assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
+    assert np.array_equal(g.log(), o.log()) and np.array_equal(g.stats()["hist"], o.stats()["hist"])
+    for d, s_o in snaps:
+        got = d.cpu().numpy() if hasattr(d, "cpu") else d
+        assert np.array_equal(got, s_o)
+    g.close()
