@@ -84,8 +84,7 @@ struct AspArgs {
   int64_t count;
   int32_t n_ev;
   int32_t tile;       // TMA form: floats per tile (multiple of 32, <= kTmaTile); set by launch_asp_replay
-  int32_t n_item;     // TMA form: gradient sources per tile, in event order (set by the launcher)
-  const float *item[kMaxItems];
+  int32_t n_item;     // TMA form: gradient sources per tile (pushes + BSP gradients; set by the launcher)
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;

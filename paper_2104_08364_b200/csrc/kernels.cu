@@ -400,8 +400,13 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   __shared__ const float *item_src[kMaxItems];
   const float lam = a.lam;
   const bool nest = a.nesterov != 0;
-  for (int k = threadIdx.x; k < a.n_item; k += blockDim.x) item_src[k] = a.item[k];
   if (threadIdx.x == 0) {
+    int k = 0;                                               // the gradient sources of one tile, in event order
+    for (int e = 0; e < a.n_ev; ++e) {
+      if (a.ev[e].kind == 0) item_src[k++] = a.ev[e].src;
+      else if (a.ev[e].kind == 2)
+        for (int j = 0; j < a.ev[e].n_src; ++j) item_src[k++] = a.bsp_src[a.ev[e].src0 + j];
+    }
     // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
     // (generic proxy): order them after the acquire
     if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -902,12 +907,8 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
   AspArgs b = a;
   b.tile = (int32_t)tile;
-  b.n_item = 0;                  // the gradient sources of one tile, in event order
-  for (int e = 0; e < a.n_ev; ++e) {
-    if (a.ev[e].kind == 0) b.item[b.n_item++] = a.ev[e].src;
-    else if (a.ev[e].kind == 2)
-      for (int k = 0; k < a.ev[e].n_src; ++k) b.item[b.n_item++] = a.bsp_src[a.ev[e].src0 + k];
-  }
+  b.n_item = 0;                  // gradient sources per tile (the kernel lists them in shared memory)
+  for (int e = 0; e < a.n_ev; ++e) b.n_item += a.ev[e].kind == 0 ? 1 : a.ev[e].kind == 2 ? a.ev[e].n_src : 0;
   const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
   if (items > kTmaStages)
     asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);

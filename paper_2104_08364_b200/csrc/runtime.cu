@@ -115,7 +115,9 @@ struct ss_ctx {
   int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed
   bool ipc_ready = false;
   int64_t inbox_slots = 0;
-  float *inbox = nullptr;              // [inbox_slots][reg_len] gradient slices owned here, written by peers
+  float *inbox = nullptr;              // [bufs][inbox_slots][reg_len] gradient slices owned here, written by peers
+  int32_t inbox_bufs = 1;              // 2: exchanges alternate between two inbox buffers (no end barrier needed)
+  int64_t xchg = 0;                    // fused exchanges issued (selects the inbox buffer)
   float *pbuf = nullptr;               // [n_hosted][P_pad] pull buffers of hosted workers, written by owners
   uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag, [160] epoch counter
   float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
@@ -464,7 +466,21 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   SS_CUDA(c, cudaStreamSynchronize(c->stream));
   close_ipc(c, false);
   slots = std::max<int64_t>(slots, std::max<int64_t>(c->n, c->max_win));
-  SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
+  // Two inbox buffers when every rank can afford them: consecutive exchanges then write different buffers, so a
+  // rank's next phase A can never overwrite slices a peer's phase B is still reading, and the phase-B kernels need no
+  // end barrier (see end_wait_needed). Any rank short of memory keeps all ranks on one buffer and end barriers.
+  int32_t two = getenv("SS_INBOX_BUFS") && getenv("SS_INBOX_BUFS")[0] == '1' ? 0 : 1;
+  if (two && cudaMalloc(&c->inbox, 2 * (size_t)slots * c->reg_len * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    c->inbox = nullptr;
+    two = 0;
+  }
+  SS_TRY(agree_all(c, &two));
+  if (!two) {
+    cudaFree(c->inbox);
+    SS_CUDA(c, cudaMalloc(&c->inbox, (size_t)slots * c->reg_len * sizeof(float)));
+  }
+  c->inbox_bufs = two ? 2 : 1;
   if (!c->pbuf) SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
   if (!c->trace_dev && getenv("SS_TRACE") && getenv("SS_TRACE")[0]) {
     c->trace_path = getenv("SS_TRACE");
@@ -545,6 +561,19 @@ ss::PeerSync peer_sync(ss_ctx *c, uint32_t wait_epoch, uint32_t signal_epoch, bo
   return p;
 }
 
+// Inbox buffer of the exchange being issued (element offset into every rank's inbox allocation).
+int64_t inbox_off(const ss_ctx *c) {
+  return c->inbox_bufs == 2 ? (c->xchg & 1) * c->inbox_slots * c->reg_len : 0;
+}
+
+// Does a phase-B kernel have to wait, at its end, until every rank finished its phase B? Only when something after
+// it on this rank's stream depends on the peers' stores being complete (a hosted pull copied out of its pull buffer),
+// when the inbox is single-buffered (the next phase A would overwrite slices still being read), or while capturing
+// (a graph replays its buffer choice, so keep the barrier).
+bool end_wait_needed(const ss_ctx *c, bool copy_follows) {
+  return copy_follows || c->inbox_bufs == 1 || c->capturing;
+}
+
 // Phase A of every fused exchange: hosted sources' owner slices -> owners' inbox slots, then signal `epoch`.
 ss_status launch_scatter(ss_ctx *c, const std::vector<std::pair<const float *, int32_t>> &src, uint32_t epoch) {
   ss::ScatterArgs a;
@@ -555,7 +584,7 @@ ss_status launch_scatter(ss_ctx *c, const std::vector<std::pair<const float *, i
     a.slot[k] = src[k].second;
     if (!aligned16(src[k].first)) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
   }
-  for (int32_t q = 0; q < c->world; ++q) a.inbox[q] = c->peer_inbox[q];
+  for (int32_t q = 0; q < c->world; ++q) a.inbox[q] = c->peer_inbox[q] + inbox_off(c);
   a.reg_len = c->reg_len;
   a.P = c->P;
   a.sync = peer_sync(c, 0, epoch, false, 0);
@@ -602,7 +631,7 @@ ss_status flush_fused(ss_ctx *c) {
     ss::AspEvent &x = a.ev[ne];
     x.kind = e.kind;
     if (e.kind == 0) {
-      x.src = host_of(c, e.worker) == me ? e.src + lo : c->inbox + (int64_t)k * c->reg_len;
+      x.src = host_of(c, e.worker) == me ? e.src + lo : c->inbox + inbox_off(c) + (int64_t)k * c->reg_len;
       x.lr = e.lr;
       x.mu = e.mu;
       vec = vec && aligned16(x.src);
@@ -622,11 +651,17 @@ ss_status flush_fused(ss_ctx *c) {
   a.count = cnt;
   a.lam = c->lam;
   a.nesterov = c->nesterov;
-  a.sync = peer_sync(c, epA, epB, true, 3);
+  bool copy_follows = false;
+  for (const Ev &e : c->win)
+    if (e.kind == 1 && e.data && host_of(c, e.worker) == me &&
+        e.dst != c->pbuf + (int64_t)(e.worker - c->first_hosted) * c->P_pad)
+      copy_follows = true;
+  a.sync = peer_sync(c, epA, epB, end_wait_needed(c, copy_follows), 3);
   Timed t;
   timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
   SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
   timed_end(c, &t);
+  c->xchg += 1;
   // gradient slots are free once the kernels that read them are done (host pulls keep theirs until their D2H)
   SS_TRY(release_slots(c, &c->win));
   for (const Ev &e : c->win) {
@@ -1173,7 +1208,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
         if (!aligned16(a.g[i])) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
       }
       sa.slot[0] = me;
-      for (int32_t q = 0; q < c->world; ++q) sa.inbox[q] = c->peer_inbox[q];
+      for (int32_t q = 0; q < c->world; ++q) sa.inbox[q] = c->peer_inbox[q] + inbox_off(c);
       sa.reg_len = c->reg_len;
       sa.P = c->P;
       sa.sync = peer_sync(c, 0, epA, false, 1);
@@ -1192,13 +1227,13 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     for (int32_t i = 0; i < k; ++i) hosted_g[i] = a.g[i];
     std::memset(a.g, 0, sizeof a.g);
     if (presum) {
-      for (int32_t q = 0; q < c->world; ++q) a.g[q] = c->inbox + (int64_t)q * c->reg_len;
+      for (int32_t q = 0; q < c->world; ++q) a.g[q] = c->inbox + inbox_off(c) + (int64_t)q * c->reg_len;
       a.n_in = c->world;
     } else {
       int32_t ni = 0, h = 0;
       for (int32_t j = 0; j < c->n; ++j) {   // the members' slices, ascending worker order
         if (!c->member[j]) continue;
-        a.g[ni++] = host_of(c, j) == me ? hosted_g[h++] + lo : c->inbox + (int64_t)j * c->reg_len;
+        a.g[ni++] = host_of(c, j) == me ? hosted_g[h++] + lo : c->inbox + inbox_off(c) + (int64_t)j * c->reg_len;
       }
       a.n_in = ni;
     }
@@ -1212,11 +1247,12 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
       for (int32_t step = 1; step < c->world; ++step)   // rotated: the ranks' stores go to distinct receivers
         a.bcast[a.n_bcast++] = c->peer_w[(me + step) % c->world] + lo;
     }
-    a.sync = peer_sync(c, epA, epB, true, 2);
+    a.sync = peer_sync(c, epA, epB, end_wait_needed(c, false), 2);
     Timed t;
     timed_begin(c, &t, 0, 4.0 * (double)cnt * (a.n_in + 4), 4.0 * (double)cnt * (c->nvls.ready ? 1 : a.n_bcast));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
+    c->xchg += 1;
   } else {
     SS_TRY(ensure_dist_buffers(c));
     if (k > 0) {
