@@ -72,8 +72,10 @@ def test_bsp_bit_exact(ss, orc, P, n, S, lam):
     for x in (g, o, o64):
         x.set_lr_schedule([2], [0.1])        # a decay boundary inside the run (version coordinate)
         x.set_lr_policy(0, lam)
+    keep = []                                 # gradients are borrowed until ss_sync (SV §8b): supersteps may be deferred
     for step in range(3):
         dg = [dev_synth(ss, j, step, P) for j in range(n)]
+        keep += dg
         hg = [host_synth(orc, j, step, P) for j in range(n)]
         perm = list(reversed(range(n)))       # order of submission must not matter (sum is ascending by id)
         g.bsp_step([dg[j] for j in perm], perm, [step] * n)
@@ -652,8 +654,10 @@ def test_max_workers_bsp(ss, orc):
     w0 = init_params(orc, P)
     g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.001, 0.9)
     o = orc.Oracle(w0, S, n, 0.001, 0.9)
+    keep = []
     for step in range(2):
         dg = [dev_synth(ss, j, step, P) for j in range(n)]
+        keep += dg                                     # borrowed until ss_sync (SV §8b)
         g.bsp_step(dg)
         assert o.bsp_step([host_synth(orc, j, step, P) for j in range(n)]) == 0
     assert np.array_equal(g.params(), o.params()) and np.array_equal(g.velocity(), o.velocity())
