@@ -51,7 +51,7 @@ SCENARIO4 = dict(n_workers=8, batch=128, total_samples=64000 * 128, quota_num=1,
 L2_BYTES = 126 * 1024 * 1024
 # ss_kernel_stats ids: 4 = the window kernel applying a BSP superstep together with the ASP events queued behind it
 # (one GPU: the superstep joins the window, see ss_bsp_step)
-KERNEL_NAMES = ["bsp_update", "asp_replay", "local_sum", "scatter", "step_window"]
+KERNEL_NAMES = ["bsp_update", "asp_replay", "local_sum", "scatter", "bsp_window"]
 METRIC = "BSP sync steps/s and ASP pushes/s at 1/2/4/8 B200; HBM & NVLink GB/s vs peak"
 UNIT = "steps/s (1 step = 1 BSP superstep + switch + n ASP push/pull + switch)"
 SEED = 20241018
@@ -218,8 +218,11 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(g.stream)
 
     class Step:
-        """One bench step through the C-ABI with prebuilt argument arrays: ss_bsp_step, ss_switch(ASP),
-        ss_asp_replay(n pushes, each followed by its pull), ss_switch(BSP) — four C calls per step.
+        """One bench step through the C-ABI with prebuilt argument arrays: ss_bsp_step, ss_flush, ss_switch(ASP),
+        ss_asp_replay(n pushes, each followed by its pull), ss_flush, ss_switch(BSP). The flushes stand for the
+        data dependencies of real training — the workers compute their first ASP gradients from the parameters after
+        the superstep, and the next superstep's gradients from the parameters after the ASP round — so the library's
+        window batching never fuses work across them (one GPU: one kernel for the superstep, one for the ASP round).
         `mark` (optional) is recorded on the library's stream between the BSP and the ASP phase."""
 
         def __init__(self, grad_src, dst_src):
@@ -242,11 +245,13 @@ def run_ours(args):
             for j in range(n):
                 self.ev[2 * j].version = ver + 1
             s = L.ss_bsp_step(c, self.gp_c, self.ws.ctypes.data, self.vs.ctypes.data, self.k)
+            s = s or L.ss_flush(c)
             if mark is not None:
                 mark.record(stream)
             s = s or L.ss_switch(c, ss.SS_ASP, 0)
             s = s or L.ss_asp_replay(c, self.ev_c, 2 * n, None)
-            s = s or L.ss_switch(c, ss.SS_BSP, 0)   # takes effect at once: flushes the ASP window
+            s = s or L.ss_flush(c)
+            s = s or L.ss_switch(c, ss.SS_BSP, 0)
             if s:
                 raise ss.SSError(s, g.last_error())
             return ver + 1 + n
@@ -255,6 +260,7 @@ def run_ours(args):
             """One BSP superstep (under BSP)."""
             self.vs[:] = ver
             s = ss.lib.ss_bsp_step(g.ctx, self.gp_c, self.ws.ctypes.data, self.vs.ctypes.data, self.k)
+            s = s or ss.lib.ss_flush(g.ctx)       # the next superstep's gradients depend on this one
             if s:
                 raise ss.SSError(s, g.last_error())
             return ver + 1
@@ -266,6 +272,7 @@ def run_ours(args):
             for j in range(n):
                 self.ev[2 * j].version = ver if first else ver - n + j + 1
             s = ss.lib.ss_asp_replay(g.ctx, self.ev_c, 2 * n, None)
+            s = s or ss.lib.ss_flush(g.ctx)       # each worker's next push depends on its pull
             if s:
                 raise ss.SSError(s, g.last_error())
             return ver + n
@@ -333,7 +340,6 @@ def run_ours(args):
     pe[0].record(stream)
     for t in range(nr):
         ver = steps_dev[t % R].bsp_only(ver)
-    g.sync()                          # one GPU: queued supersteps are applied by window kernels; launch the last one
     pe[1].record(stream)
     barrier()
     g.switch(ss.SS_ASP, 0)
@@ -353,9 +359,9 @@ def run_ours(args):
              "asp_pushes_per_s": n * nr / (asp_only_ms / 1e3), "asp_us_per_window": 1e3 * asp_only_ms / nr,
              "supersteps": nr, "windows": nr, "pushes_per_window": n,
              "note": "pure BSP supersteps back to back, then pure ASP windows (n pushes, each followed by its pull) "
-                     "back to back; two CUDA events per run, no per-launch instrumentation; max over ranks. One GPU: "
-                     "back-to-back supersteps share window kernels (up to 128 gradients per launch), so w and v "
-                     "cross HBM once per window instead of once per superstep"}
+                     "back to back; two CUDA events per run, no per-launch instrumentation; max over ranks. Every "
+                     "superstep and every window is flushed (issued as its own kernel), as the data dependencies of "
+                     "real training force"}
     ver = g.version
     st = g.stats(64)
     assert st["status"] == 0 and g.sync_status() == 0, g.last_error()
@@ -465,13 +471,15 @@ def run_ours(args):
                 kernels[name]["nvlink_frac_of_770"] = round(k["nvlink_bytes"] / sec / 1e9 / nvl_peak, 4)
 
     steps_per_s = args.steps / (total_ms / 1e3)
-    # 1-GPU form: n BSP + n ASP gradients read, n pulls written, w and v read and written once (one window kernel)
-    step_bytes = (3 * n + 4) * 4 * P / world
+    # 1-GPU form: n BSP + n ASP gradients read, n pulls written, w and v read and written by each of the two kernels
+    step_bytes = (3 * n + 8) * 4 * P / world
     if world == 1:
-        phases = {"profiled_ms_per_step": prof_ms / args.steps,
-                  "note": "one GPU: the BSP superstep is applied by the same window kernel as the ASP round behind it "
-                          "(one launch per step), so the step has no separately timed BSP phase; pure-protocol rates "
-                          "are in protocol_rates"}
+        phases = {"bsp_steps_per_s": args.steps / (bsp_ms / 1e3), "asp_pushes_per_s": n * args.steps / (asp_ms / 1e3),
+                  "bsp_ms_per_step": bsp_ms / args.steps, "asp_ms_per_round": asp_ms / args.steps,
+                  "profiled_ms_per_step": prof_ms / args.steps,
+                  "note": "from the profiled pass (events at every launch and phase boundary); one GPU: the superstep "
+                          "runs in the window kernel (bsp_window: a window holding one BSP event), the ASP round in "
+                          "asp_replay"}
     else:
         phases = {"bsp_steps_per_s": args.steps / (bsp_ms / 1e3), "asp_pushes_per_s": n * args.steps / (asp_ms / 1e3),
                   "bsp_ms_per_step": bsp_ms / args.steps, "asp_ms_per_round": asp_ms / args.steps,

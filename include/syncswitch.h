@@ -213,6 +213,13 @@ ss_status ss_asp_replay(ss_ctx *ctx, const ss_event *ev, int64_t n_ev, int64_t *
  * including a fused-path cross-GPU wait that timed out). Not allowed while capturing a graph (SS_E_STATE). */
 ss_status ss_sync(ss_ctx *ctx);
 
+/* Issue the device work of the calls accepted so far (the pending window, including one-GPU supersteps deferred into
+ * it) on the context's stream, without waiting. A caller whose next inputs depend on these results (a worker that
+ * computes its next gradient from a pulled snapshot, or from the parameters after a superstep) flushes, then orders
+ * its own stream after the context's (ss_wait_stream) — the window batching never reaches across such a dependency.
+ * Buffers stay BORROWED until ss_sync. Collective when distributed. Errors: SS_E_DIVERGED, SS_E_CUDA, SS_E_NCCL. */
+ss_status ss_flush(ss_ctx *ctx);
+
 /* Copies the unpadded parameters w (fp32[n_params]) / momentum v to a HOST buffer (collective when distributed).
  * Flushes and synchronizes first. */
 ss_status ss_read_params(ss_ctx *ctx, float *host_dst);

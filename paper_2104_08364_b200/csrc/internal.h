@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "syncswitch.h"
+
 namespace ss {
 
 constexpr int kMaxWorkers = 256;  // SV §8b: workers in [1, 256]
@@ -85,6 +87,7 @@ struct AspArgs {
   int32_t n_ev;
   int32_t tile;       // TMA form: floats per tile (multiple of 32, <= kTmaTile); set by launch_asp_replay
   int32_t n_item;     // TMA form: gradient sources per tile (pushes + BSP gradients; set by the launcher)
+  int32_t stages;     // TMA form: ring depth in tiles (set by the launcher)
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;
@@ -131,4 +134,6 @@ cudaError_t launch_softmax_grad(const float *X, const int32_t *y, int32_t B, int
 struct ss_ctx;
 namespace ss {
 CtxInfo ctx_info(const ss_ctx *c);
+// Launches the pending window (the device work of already accepted calls); no-op when nothing is pending.
+ss_status ctx_flush(ss_ctx *c);
 }  // namespace ss

@@ -355,10 +355,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_scalar_kernel(const __gri
 #ifndef SS_TMA_STAGES
 #define SS_TMA_STAGES 10   // 80 KB rings -> 2 CTAs per SM: 96.5-98% of the HBM copy vs 93% at 6 stages / 4 CTAs
 #endif                     // (profiles/r01_replay_sweep.txt)
-constexpr int kTmaTile = SS_TMA_TILE;                // floats per tile: 256 threads x 2 float4
+constexpr int kTmaTile = SS_TMA_TILE;                // floats per tile (max): 256 threads x 2 float4
 constexpr int kTmaStages = SS_TMA_STAGES;
 constexpr int kTmaSmem = kTmaStages * kTmaTile * 4;  // 80 KB of dynamic shared memory
 constexpr int kTU = kTmaTile / (4 * kThreads);       // float4 per thread per tile
+constexpr int kMaxStages = kMaxItems;                // ring stages (runtime; the small-launch form holds every item)
+constexpr int kTmaSmemMax = 200 * 1024;              // dynamic shared memory the launcher may ask for
 static_assert(kTU >= 1 && kTmaTile % (4 * kThreads) == 0, "tile must be a multiple of 4 x kThreads floats");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -389,15 +391,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // kRefill = false: every CTA's items (tiles x gradient sources) fit the ring, so no stage is ever reused and the
 // per-item CTA barrier is dropped (small P; a separate instantiation because a runtime-conditional barrier costs the
-// large-P loop 2.5%: profiles/r01_replay_condsync.txt).
+// large-P loop 2.5%: profiles/r01_replay_condsync.txt). Tile length (a.tile floats) and ring depth (a.stages) are
+// chosen per launch: the streaming form uses kTmaTile-float tiles and a kTmaStages ring; a launch smaller than a few
+// waves of it (config 2) uses one shorter tile per CTA and a ring deep enough for all of that tile's gradient sources,
+// so every CTA issues all its bulk copies at once and never waits on a CTA barrier.
 // Window events: push (one staged gradient tile), BSP superstep (n_src staged tiles summed in ascending worker order
 // into a register accumulator, then the mean and the momentum update), pull (store of the current w).
 template <bool kRefill>
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
   const Ep ep = peer_enter(a.sync);
   extern __shared__ __align__(128) float ring[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ const float *item_src[kMaxItems];
+  // ring depth and tile length: compile-time in the streaming (refill) form, per launch in the small-launch form
+  const int n_stage = kRefill ? kTmaStages : a.stages;      // (<= kMaxStages)
   const float lam = a.lam;
   const bool nest = a.nesterov != 0;
   if (threadIdx.x == 0) {
@@ -410,43 +417,58 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
     // (generic proxy): order them after the acquire
     if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < n_stage; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int n_item = a.n_item;                               // gradient sources per tile, in event order
   const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
-  const int64_t tsz = a.tile;                                // floats per tile (<= kTmaTile)
+  const int64_t tsz = kRefill ? (int64_t)kTmaTile : (int64_t)a.tile;   // floats per tile (<= kTmaTile)
   const int64_t n_tiles = (nvec + tsz - 1) / tsz;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * n_item;                   // one gradient tile per (tile, source)
 
-  auto issue = [&](int64_t it) {                             // thread 0: stage the gradient tile of item `it`
-    const int64_t tile = blockIdx.x + (it / n_item) * gridDim.x;
-    const int64_t off = tile * tsz;
+  // Items are staged and consumed in order, so both sides walk cursors instead of dividing by the runtime ring depth
+  // and source count: the producer (thread 0) keeps (tile, source, stage) of the next item to issue; every thread
+  // keeps (stage, parity) of the next item to consume.
+  int64_t p_next = 0, p_tile = blockIdx.x;                   // producer cursor (thread 0 only)
+  int p_src = 0, p_stage = 0;
+  auto issue_next = [&]() {                                  // thread 0: stage the gradient tile of item p_next
+    const int64_t off = p_tile * tsz;
     const int64_t len = min(tsz, nvec - off);
-    const int s = (int)(it % kTmaStages);
-    mbar_expect_tx(&full[s], (uint32_t)(len * 4));
-    bulk_g2s(ring + s * kTmaTile, item_src[it % n_item] + off, (uint32_t)(len * 4), &full[s]);
+    mbar_expect_tx(&full[p_stage], (uint32_t)(len * 4));
+    bulk_g2s(ring + p_stage * tsz, item_src[p_src] + off, (uint32_t)(len * 4), &full[p_stage]);
+    ++p_next;
+    if (++p_src == n_item) {
+      p_src = 0;
+      p_tile += gridDim.x;
+    }
+    if (++p_stage == n_stage) p_stage = 0;
   };
   if (threadIdx.x == 0)
-    for (int64_t it = 0; it < items && it < kTmaStages; ++it) issue(it);
-  // wait for item `it` and hand back its stage: returns the thread's float4 u of the staged tile
-  auto staged = [&](int64_t it, int u) -> float4 {
-    return *reinterpret_cast<const float4 *>(ring + (int)(it % kTmaStages) * kTmaTile + 4 * (threadIdx.x + u * kThreads));
+    while (p_next < items && p_next < n_stage) issue_next();
+  int c_stage = 0;                                           // consumer cursor: stage and parity of item `it`
+  uint32_t c_phase = 0;
+  auto wait_item = [&]() { mbar_wait(&full[c_stage], c_phase); };
+  // the thread's float4 u of the staged tile of the item being consumed
+  auto staged = [&](int u) -> float4 {
+    return *reinterpret_cast<const float4 *>(ring + c_stage * tsz + 4 * (threadIdx.x + u * kThreads));
   };
-  auto release = [&](int64_t it) {
-    if (kRefill) {                                          // (a window that fits the ring never reuses a stage)
-      __syncthreads();                                      // every thread is done with the stage of item `it`
-      if (threadIdx.x == 0 && it + kTmaStages < items) {
+  auto release = [&]() {                                     // done with the item being consumed; advance
+    if (kRefill) {                                           // (a window that fits the ring never reuses a stage)
+      __syncthreads();                                       // every thread is done with this stage
+      if (threadIdx.x == 0 && p_next < items) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(it + kTmaStages);
+        issue_next();                                        // refills exactly this stage (p_next = it + n_stage)
       }
+    }
+    if (++c_stage == n_stage) {
+      c_stage = 0;
+      c_phase ^= 1u;
     }
   };
 
   bool bad = false;
-  int64_t it = 0;
   for (int64_t tl = 0; tl < my_tiles; ++tl) {
     const int64_t off = (blockIdx.x + tl * gridDim.x) * tsz;
     const int64_t len = min(tsz, nvec - off);
@@ -464,12 +486,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     for (int e = 0; e < a.n_ev; ++e) {
       const int kind = a.ev[e].kind;
       if (kind == 0) {
-        mbar_wait(&full[(int)(it % kTmaStages)], (uint32_t)((it / kTmaStages) & 1));
+        wait_item();
         const float neg_eta = -a.ev[e].lr, mu = a.ev[e].mu;
 #pragma unroll
         for (int u = 0; u < kTU; ++u) {
           if (!ok[u]) continue;
-          float4 g = staged(it, u);
+          float4 g = staged(u);
           float *gp = &g.x, *wp = &wv[u].x, *vp = &vv[u].x;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -479,21 +501,19 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
             wp[c] = __fmaf_rn(neg_eta, nest ? __fmaf_rn(mu, vp[c], gg) : vp[c], wp[c]);
           }
         }
-        release(it);
-        ++it;
+        release();
       } else if (kind == 2) {
         float4 acc[kTU];
         const int ns = a.ev[e].n_src;
         for (int k = 0; k < ns; ++k) {
-          mbar_wait(&full[(int)(it % kTmaStages)], (uint32_t)((it / kTmaStages) & 1));
+          wait_item();
 #pragma unroll
           for (int u = 0; u < kTU; ++u) {
             if (!ok[u]) continue;
-            const float4 g = staged(it, u);
+            const float4 g = staged(u);
             acc[u] = k == 0 ? g : add4(acc[u], g);            // ascending worker order (reading C12)
           }
-          release(it);
-          ++it;
+          release();
         }
         const float dv = a.ev[e].divisor;
         const Upd up{dv, 1.0f / dv, a.ev[e].mu, -a.ev[e].lr, lam, is_pow2(dv), nest};
@@ -892,23 +912,42 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
     return cudaGetLastError();
   }
-  static const int r = [] {    // resident CTAs per SM at this kernel's shared memory (thread-safe static init)
+  static const int r = [] {    // resident CTAs per SM at the streaming form's shared memory (thread-safe static init)
     int res = 0;
-    cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
+    cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, asp_replay_tma_kernel<true>, kThreads, kTmaSmem);
     return res > 0 ? res : 1;
   }();
-  // grid-stride over fixed kTmaTile tiles, at most one wave of resident CTAs
   const int64_t nvec = (a.count >> 2) << 2;
+  AspArgs b = a;
+  b.n_item = 0;                  // gradient sources per tile (the kernel lists them in shared memory)
+  for (int e = 0; e < a.n_ev; ++e) b.n_item += a.ev[e].kind == 0 ? 1 : a.ev[e].kind == 2 ? a.ev[e].n_src : 0;
+  // Small-launch form: one tile per CTA, every gradient source of it staged at once (no stage reuse, no CTA
+  // barrier per item), as many CTAs as fit (up to 4 per SM at 64 registers x 256 threads); tiles are a multiple of
+  // 32 floats (128 B). Used when such a tile is no longer than the streaming form's.
+  static const bool small_form = !(getenv("SS_REPLAY_STREAMING") && getenv("SS_REPLAY_STREAMING")[0] == '1');
+  if (small_form && b.n_item > 0 && b.n_item <= kMaxStages) {
+    for (int per_sm = 4; per_sm >= 1; --per_sm) {
+      const int64_t want = (int64_t)per_sm * num_sms();
+      const int64_t t = std::max<int64_t>(32, ((nvec + want - 1) / want + 31) / 32 * 32);
+      if (t > kTmaTile) break;
+      const int64_t smem = (int64_t)b.n_item * t * 4;
+      if (smem > kTmaSmemMax || per_sm * (smem + 5 * 1024) > 228 * 1024) continue;   // + static smem + reserve
+      b.tile = (int32_t)t;
+      b.stages = b.n_item;
+      const int64_t grid = std::max<int64_t>(1, (nvec + t - 1) / t);
+      asp_replay_tma_kernel<false><<<(int)grid, kThreads, (size_t)smem, s>>>(b);
+      return cudaGetLastError();
+    }
+  }
+  // streaming form: grid-stride over kTmaTile tiles, at most one wave of resident CTAs, a kTmaStages-tile ring
   const int64_t slots = (int64_t)r * num_sms();
   const int64_t tile = kTmaTile;
   const int64_t tiles = (nvec + tile - 1) / tile;
   const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
-  AspArgs b = a;
   b.tile = (int32_t)tile;
-  b.n_item = 0;                  // gradient sources per tile (the kernel lists them in shared memory)
-  for (int e = 0; e < a.n_ev; ++e) b.n_item += a.ev[e].kind == 0 ? 1 : a.ev[e].kind == 2 ? a.ev[e].n_src : 0;
+  b.stages = kTmaStages;
   const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
   if (items > kTmaStages)
     asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);

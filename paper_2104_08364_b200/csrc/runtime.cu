@@ -1372,6 +1372,11 @@ ss_status ss_sync(ss_ctx *c) {
   return sync_impl(c);
 }
 
+ss_status ss_flush(ss_ctx *c) {
+  SS_TRY(check_live(c));
+  return flush(c);
+}
+
 // ---------------------------------------------------------------------------------------------------------------
 // CUDA-graph capture of one step (latency-bound small models). The device work the calls
 // between begin and end enqueue is recorded (not executed) into a graph; replay launches it K times and applies
@@ -1628,5 +1633,10 @@ CtxInfo ctx_info(const ss_ctx *c) {
   i.fused = c->fused_mode != 0;
   i.stream = c->stream;
   return i;
+}
+
+ss_status ctx_flush(ss_ctx *c) {
+  SS_TRY(check_live(c));
+  return flush(c);
 }
 }  // namespace ss

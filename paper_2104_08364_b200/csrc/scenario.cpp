@@ -157,6 +157,11 @@ extern "C" ss_status ss_scenario_run(ss_ctx *ctx, const ss_scenario *sc, ss_scen
       std::vector<const float *> g;
       std::vector<int32_t> ws;
       std::vector<int64_t> vs;
+      // one GPU defers a superstep into the pending window: launch it before its gradient buffers are rewritten
+      if (ctx) {
+        ss_status s = ss::ctx_flush(ctx);
+        if (s != SS_OK) return s;
+      }
       for (int32_t j = 0; j < n; ++j) {
         if (!mem[j] || !hosted(j)) continue;
         ss_status s = gen(j, ctx ? buf.bsp[j] : nullptr);

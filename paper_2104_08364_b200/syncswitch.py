@@ -27,7 +27,7 @@ STATUS = ["SS_OK", "SS_E_INVAL", "SS_E_STATE", "SS_E_PROTOCOL", "SS_E_BARRIER", 
 # every symbol include/syncswitch.h declares (tests check the library exports each one)
 EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_last_error", "ss_set_lr_schedule",
            "ss_set_lr_policy", "ss_current_lr", "ss_bsp_step", "ss_asp_push", "ss_pull", "ss_switch",
-           "ss_asp_replay", "ss_sync", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
+           "ss_asp_replay", "ss_sync", "ss_flush", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
            "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_set_nesterov", "ss_get_exchange", "ss_pull_buffer",
@@ -100,6 +100,7 @@ def _load():
         "ss_switch": [p, i32, i64],
         "ss_asp_replay": [p, p, i64, p],
         "ss_sync": [p],
+        "ss_flush": [p],
         "ss_read_params": [p, p],
         "ss_read_velocity": [p, p],
         "ss_get_stats": [p, p, p, p, i32, p],
@@ -227,6 +228,10 @@ def ss_asp_replay(ctx, events):
 
 def ss_sync(ctx) -> int:
     return lib.ss_sync(ctx)
+
+
+def ss_flush(ctx) -> int:
+    return lib.ss_flush(ctx)
 
 
 def ss_read_params(ctx, n_params: int):
@@ -509,6 +514,9 @@ class SyncSwitch:
 
     def sync(self):
         return self._chk(ss_sync(self.ctx))
+
+    def flush(self):
+        return self._chk(ss_flush(self.ctx))
 
     def sync_status(self) -> int:
         return ss_sync(self.ctx)

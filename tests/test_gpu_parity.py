@@ -666,13 +666,14 @@ def test_max_workers_bsp(ss, orc):
 
 
 # ---------------------------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("mode", ["device", "unaligned", "host"])
+@pytest.mark.parametrize("mode", ["device", "unaligned", "host", "flushed"])
 @pytest.mark.parametrize("P,n,S,window", [(100003, 8, 8, 16), (4099, 3, 2, 5), (2 ** 20 + 3, 8, 8, 64)])
 def test_windows_with_bsp_supersteps(ss, orc, mode, P, n, S, window):
     """One GPU: BSP supersteps join the pending window (one kernel applies supersteps, pushes and pulls tile by tile,
     w and v on chip). A long program without sync points — 20 supersteps (crossing the window's 128-gradient cap at
     n = 8), a switch, a seeded ASP phase with pulls, a switch back, more supersteps, an lr boundary inside — is
-    bit-identical to the oracle for device, unaligned (scalar kernel) and host (staged) gradients."""
+    bit-identical to the oracle for device, unaligned (scalar kernel) and host (staged) gradients, and with ss_flush
+    after every call (every superstep and push its own kernel: the bench's form)."""
     w0 = init_params(orc, P)
     g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
@@ -697,6 +698,8 @@ def test_windows_with_bsp_supersteps(ss, orc, mode, P, n, S, window):
         gs = [grad(j) for j in range(n)]
         v = o.version
         g.bsp_step([x[0] for x in gs], list(range(n)), [v] * n)
+        if mode == "flushed":
+            g.flush()                     # ss_flush: issue the device work now (the bench's dependency points)
         assert o.bsp_step([x[1] for x in gs]) == 0
 
     for _ in range(20):
@@ -715,6 +718,8 @@ def test_windows_with_bsp_supersteps(ss, orc, mode, P, n, S, window):
         else:
             d, h = grad(j)
             sg = g.asp_push(j, d, base_g[j])
+            if mode == "flushed":
+                g.flush()
             rc, so = o.asp_push(j, h, base_o[j])
             assert rc == 0 and sg == so
     g.switch(BSP, 0)
