@@ -407,26 +407,64 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   const int n_stage = kRefill ? kTmaStages : a.stages;      // (<= kMaxStages)
   const float lam = a.lam;
   const bool nest = a.nesterov != 0;
-  if (threadIdx.x == 0) {
-    int k = 0;                                               // the gradient sources of one tile, in event order
-    for (int e = 0; e < a.n_ev; ++e) {
-      if (a.ev[e].kind == 0) item_src[k++] = a.ev[e].src;
-      else if (a.ev[e].kind == 2)
-        for (int j = 0; j < a.ev[e].n_src; ++j) item_src[k++] = a.bsp_src[a.ev[e].src0 + j];
-    }
-    // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this thread acquired
-    // (generic proxy): order them after the acquire
-    if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int s = 0; s < n_stage; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   const int n_item = a.n_item;                               // gradient sources per tile, in event order
   const int64_t nvec = (a.count >> 2) << 2;                  // elements covered by 16-byte tiles
   const int64_t tsz = kRefill ? (int64_t)kTmaTile : (int64_t)a.tile;   // floats per tile (<= kTmaTile)
   const int64_t n_tiles = (nvec + tsz - 1) / tsz;
   const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_tiles * n_item;                   // one gradient tile per (tile, source)
+
+  // w and v of the CTA's current tile live in registers; the first tile's loads are issued before the prologue so
+  // their latency overlaps it, each later tile's right after the previous one is stored
+  float4 wv[kTU], vv[kTU];
+  bool ok[kTU];
+  auto load_wv = [&](int64_t tl) {
+    const int64_t off = (blockIdx.x + tl * gridDim.x) * tsz;
+    const int64_t len = min(tsz, nvec - off);
+#pragma unroll
+    for (int u = 0; u < kTU; ++u) {
+      const int64_t i = 4 * (threadIdx.x + u * kThreads);    // element within the tile
+      ok[u] = i < len;
+      if (ok[u]) {
+        wv[u] = ld4(a.w + off + i);
+        vv[u] = ld4(a.v + off + i);
+      }
+    }
+  };
+  if (my_tiles > 0) load_wv(0);
+
+  // Prologue, warp 0: list the gradient sources of a tile in event order (lane l takes events l and l + 32; their
+  // item offsets are a warp prefix sum of the per-event source counts) and initialise the ring's barriers.
+  static_assert(kMaxEvents <= 64, "two events per lane");
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    auto count_of = [&](int e) {
+      return e < a.n_ev ? (a.ev[e].kind == 0 ? 1 : a.ev[e].kind == 2 ? a.ev[e].n_src : 0) : 0;
+    };
+    const int c0 = count_of(lane), c1 = count_of(lane + 32);
+    int s0 = c0, s1 = c1;                                    // inclusive scans over the lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t0 = __shfl_up_sync(0xffffffffu, s0, d), t1 = __shfl_up_sync(0xffffffffu, s1, d);
+      if (lane >= d) {
+        s0 += t0;
+        s1 += t1;
+      }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, s0, 31);
+    auto list = [&](int e, int pos, int cnt) {
+      for (int k = 0; k < cnt; ++k)
+        item_src[pos + k] = a.ev[e].kind == 0 ? a.ev[e].src : a.bsp_src[a.ev[e].src0 + k];
+    };
+    list(lane, s0 - c0, c0);
+    list(lane + 32, tot0 + s1 - c1, c1);
+    for (int st = lane; st < n_stage; st += 32) mbar_init(&full[st], 1);
+    // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this CTA acquired
+    // (generic proxy): order them after the acquire
+    if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   // Items are staged and consumed in order, so both sides walk cursors instead of dividing by the runtime ring depth
   // and source count: the producer (thread 0) keeps (tile, source, stage) of the next item to issue; every thread
@@ -445,8 +483,17 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     }
     if (++p_stage == n_stage) p_stage = 0;
   };
-  if (threadIdx.x == 0)
-    while (p_next < items && p_next < n_stage) issue_next();
+  if (kRefill) {
+    if (threadIdx.x == 0)
+      while (p_next < items && p_next < n_stage) issue_next();
+  } else if (threadIdx.x < 32) {                             // the ring holds every item: warp 0 issues them all
+    for (int64_t it = threadIdx.x; it < items; it += 32) {
+      const int64_t off = (blockIdx.x + (it / n_item) * gridDim.x) * tsz;
+      const int64_t len = min(tsz, nvec - off);
+      mbar_expect_tx(&full[it], (uint32_t)(len * 4));
+      bulk_g2s(ring + it * tsz, item_src[it % n_item] + off, (uint32_t)(len * 4), &full[it]);
+    }
+  }
   int c_stage = 0;                                           // consumer cursor: stage and parity of item `it`
   uint32_t c_phase = 0;
   auto wait_item = [&]() { mbar_wait(&full[c_stage], c_phase); };
@@ -471,18 +518,6 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   bool bad = false;
   for (int64_t tl = 0; tl < my_tiles; ++tl) {
     const int64_t off = (blockIdx.x + tl * gridDim.x) * tsz;
-    const int64_t len = min(tsz, nvec - off);
-    float4 wv[kTU], vv[kTU];
-    bool ok[kTU];
-#pragma unroll
-    for (int u = 0; u < kTU; ++u) {
-      const int64_t i = 4 * (threadIdx.x + u * kThreads);    // element within the tile
-      ok[u] = i < len;
-      if (ok[u]) {
-        wv[u] = ld4(a.w + off + i);
-        vv[u] = ld4(a.v + off + i);
-      }
-    }
     for (int e = 0; e < a.n_ev; ++e) {
       const int kind = a.ev[e].kind;
       if (kind == 0) {
@@ -540,6 +575,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
       st4(a.w + i, wv[u]);
       st4(a.v + i, vv[u]);
     }
+    if (tl + 1 < my_tiles) load_wv(tl + 1);
   }
   // scalar tail (count % 4 elements), first CTA
   if (blockIdx.x == 0) {

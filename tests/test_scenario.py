@@ -133,14 +133,22 @@ def test_elastic_scenario_on_gpu_bit_exact(ss, orc):
                                    slow_t0=10000, slow_t1=60000))
 
 
-def _scenario_on_gpu(ss, orc, sc):
+@pytest.mark.gpu
+def test_scenario_on_gpu_config2_shape(ss, orc):
+    """The straggler scenario at the ResNet-32 shape (P = 464,154, n = S = 8: SV §8(d) config 4 "or 464,154"), a
+    shortened workload that still detects the straggler, switches to ASP and back: bit-exact with the oracle."""
+    _scenario_on_gpu(ss, orc, dict(BASE, total_samples=1200 * 128, quota_num=1, quota_den=2, slow_t0=5000,
+                                   slow_t1=45000), P=464154, S=8)
+
+
+def _scenario_on_gpu(ss, orc, sc, P=4099, S=4):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    P, n = 4099, sc["n_workers"]
+    n = sc["n_workers"]
     w0 = orc.synth_grad(20241019, 255, 0, 0, P) * np.float32(64.0)
-    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), 4, n, 0.1, 0.9)
-    o = orc.Oracle(w0, 4, n, 0.1, 0.9)
+    g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
     s, log_g, res_g = ss.ss_scenario_run(g.ctx, sc)
     assert s == 0, g.last_error()
     log_o, res_o = orc.scenario(sc, o, P)
