@@ -87,8 +87,8 @@ def parse():
     ap.add_argument("--scenario-samples", type=int, default=16000 * 128,
                     help="config 4: total samples W of the scenario (the paper's 64K x 128 takes minutes)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--fused", default="auto", choices=["auto", "0", "1", "2"],
-                    help="G>1 exchange: 0 NCCL, 1 fused exact, 2 fused pre-summed; auto = 1 if n <= G else 2")
+    ap.add_argument("--fused", default="auto", choices=["auto", "0", "1", "2", "3"],
+                    help="G>1 exchange: 0 NCCL, 1 fused exact, 2 fused pre-summed, 3 fused pull; auto = 3 if n <= G else 2")
     ap.add_argument("--workload", action="store_true",
                     help="config 2/3: sync-only time of the whole 64K-iteration workload, pure BSP / pure ASP / "
                          "switched (Table I remap)")
@@ -194,7 +194,9 @@ def run_ours(args):
         uid = [ss.ss_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         g.init_dist(rank, world, uid[0])
-    fused = (1 if n <= world else 2) if args.fused == "auto" else int(args.fused)
+    # exchange: one worker per GPU or fewer (the paper's layout) -> the one-kernel pull exchange (mode 3); more workers
+    # than GPUs -> each rank pre-sums its workers and scatters one slice per owner (mode 2)
+    fused = (3 if n <= world else 2) if args.fused == "auto" else int(args.fused)
     if world > 1:
         g.set_fused(fused)
     g.set_window(win)
@@ -208,6 +210,11 @@ def run_ours(args):
     set_bytes = 2 * max(len(hosted), 1) * 4 * P
     R = max(1, math.ceil(3 * L2_BYTES / set_bytes))
     ring = {(j, r): torch.empty(P, device="cuda") for j in hosted for r in range(2 * R)}
+    if world > 1 and fused == 3 and R == 1:
+        # mode 3 reads superstep gradients in place from the exported gradient buffers: the worker writes its
+        # gradient there (zero copy). With R > 1 sets the sets stay separate buffers, copied in per superstep.
+        for j in hosted:
+            ring[(j, 0)] = g.grad_buffer(j)
     for (j, r), buf in ring.items():
         ss.ss_check(ss.ss_synth_grad(SEED, j, r % 2, 0, P, buf))   # every set holds the same values (k = 0, 1)
     if world > 1 and fused:
@@ -404,8 +411,12 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         hring = {(j, r): torch.empty(P, pin_memory=True) for j in hosted for r in range(2)}
-        for key, buf in hring.items():
-            buf.copy_(ring[key])
+        tmpd = torch.empty(P, device="cuda")
+        for (j, r), buf in hring.items():          # the same values as the device ring (k = 0: BSP, k = 1: ASP)
+            ss.ss_check(ss.ss_synth_grad(SEED, j, r, 0, P, tmpd))
+            torch.cuda.synchronize()
+            buf.copy_(tmpd)
+        del tmpd
         hdst = {j: torch.empty(P, pin_memory=True) for j in hosted}
         del ring
         torch.cuda.empty_cache()
@@ -501,7 +512,8 @@ def run_ours(args):
         "config": {"workload": cfg["name"], "P": P, "n_workers": n, "n_shards": S, "asp_window_events": win,
                    "parallelism": f"sharded PS over {world} GPU(s)",
                    "exchange": "single GPU" if world == 1 else
-                   ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed"][fused],
+                   ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed",
+                    "fused one-kernel pull (gradient buffers read in place over NVLink)"][fused],
                    "gradient_sets": R,
                    "l2": (f"inputs larger than L2: {step_bytes / 1e9:.2f} GB streamed per step vs 126 MB L2, no flush"
                           if R == 1 else
@@ -720,7 +732,9 @@ def run_workload(args):
     cfg, wl = CONFIGS[args.config], WORKLOADS[args.config]
     P, n, S, win = cfg["P"], cfg["n"], cfg["S"], args.window or cfg["window"]
     hosted = [j for j in range(n) if (j * world) // n == rank]
-    fused = (1 if n <= world else 2) if args.fused == "auto" else int(args.fused)
+    # exchange: one worker per GPU or fewer (the paper's layout) -> the one-kernel pull exchange (mode 3); more workers
+    # than GPUs -> each rank pre-sums its workers and scatters one slice per owner (mode 2)
+    fused = (3 if n <= world else 2) if args.fused == "auto" else int(args.fused)
     w0 = torch.empty(P, device="cuda")
     ss.ss_check(ss.ss_synth_grad(SEED + 1, 255, 0, 0, P, w0))
     w0.mul_(64.0)
@@ -776,6 +790,7 @@ def run_workload(args):
             vs[:] = t
             st = L.ss_bsp_step(c, ctypes.cast(gp[t % 2], ctypes.c_void_p), ws.ctypes.data, vs.ctypes.data,
                                len(hosted))
+            st = st or L.ss_flush(c)         # the next superstep's gradients depend on this one
             if st:
                 raise ss.SSError(st, g.last_error())
         if n_asp:
@@ -817,7 +832,8 @@ def run_workload(args):
                                                  f"s={wl['s'][0]}/{wl['s'][1]} (Table I remap)",
                        "P": P, "n_workers": n, "n_shards": S, "asp_window_events": win,
                        "exchange": "single GPU" if world == 1 else
-                       ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed"][fused],
+                       ["NCCL RS/AG + send/recv", "fused peer-memory, exact", "fused peer-memory, pre-summed",
+                    "fused one-kernel pull (gradient buffers read in place over NVLink)"][fused],
                        "schedule": "ss_schedule, period 1000 ticks, jitter 100, seed 7; each push followed by its pull"},
             "runs": runs,
             "speedup_vs_bsp": {k: runs["bsp"]["seconds"] / r["seconds"] for k, r in runs.items()},

@@ -90,9 +90,16 @@ ss_status ss_init_dist(ss_ctx *ctx, int32_t rank, int32_t world, const void *ncc
  *      hang). At most 8 ranks.
  *   2  fused peer memory, pre-summed: as 1, but each rank first sums its hosted workers and sends one slice per
  *      owner (fewer NVLink bytes when n > world; summation order: ascending within a rank, then ascending ranks).
- * In modes 1 and 2 the BSP broadcast of the updated slices uses NVSwitch multicast (NVLS, one multimem.st per
- * element reaches every replica) when world >= 8 and the driver supports it, else P2P stores; environment variable
- * SS_NVLS=0/1 overrides. Errors: SS_E_INVAL. */
+ *   3  fused pull (BSP supersteps in ONE kernel per rank): every hosted gradient sits in the
+ *      rank's exported gradient buffer of its worker (ss_grad_buffer: zero copy; any other buffer — device or host —
+ *      is copied into it on the context's stream first); each owner loads its region of every member's gradient
+ *      (hosted ones from local HBM, the others over NVLink), sums them in ascending worker order (bit-identical to
+ *      one GPU), updates w and v and stores the new slice into every replica, between a cross-GPU barrier at kernel
+ *      entry and one at exit. ASP windows run as in mode 1. Moves the fewest NVLink bytes when every rank hosts at
+ *      most one worker (n <= world, the paper's one-PS-per-worker-node layout).
+ * In modes 1, 2 and 3 the BSP broadcast of the updated slices uses P2P stores at every world size; environment variable
+ * SS_NVLS=1 switches it to NVSwitch multicast (NVLS, one multimem.st per element reaches every replica; opt-in: no
+ * speed-up measured at 2 or 4 GPUs). Errors: SS_E_INVAL. */
 ss_status ss_set_fused(ss_ctx *ctx, int32_t mode);
 
 /* The exchange in effect: *mode = the ss_set_fused mode (0 on a single GPU), *nvls = 1 once the fused path has set up
@@ -105,6 +112,13 @@ ss_status ss_get_exchange(ss_ctx *ctx, int32_t *mode, int32_t *nvls);
  * it as ss_pull's dst makes the pull zero-copy (otherwise the snapshot is copied from it into dst). Collective on
  * first use. Errors: SS_E_INVAL (worker not hosted here), SS_E_STATE (single GPU or NCCL mode). */
 ss_status ss_pull_buffer(ss_ctx *ctx, int32_t worker, float **out);
+
+/* Fused multi-GPU mode: the CUDA-IPC-mapped gradient buffer (device fp32[P_pad], owned by the context, valid until
+ * ss_destroy; the padding past n_params must stay 0) of a worker hosted on this rank. In mode 3 owners load their
+ * region of it over NVLink during a superstep: a worker that writes its gradient here and passes this pointer to
+ * ss_bsp_step saves the copy-in. Like every gradient it is BORROWED by the superstep until ss_sync. Collective on
+ * first use. Errors: SS_E_INVAL (worker not hosted here), SS_E_STATE (single GPU or NCCL mode). */
+ss_status ss_grad_buffer(ss_ctx *ctx, int32_t worker, float **out);
 
 /* Fills the 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
 ss_status ss_nccl_unique_id(void *out128);

@@ -24,6 +24,8 @@ struct PeerSync {
   // CTA to the signalled epoch), so a captured CUDA graph replays with fresh epochs every time.
   uint32_t *epoch_base;
   int32_t has_wait;                 // every CTA waits for flag >= base + wait_off from all ranks before starting
+  int32_t entry_signal;             // ... after signalling base + wait_off to every rank itself (the inputs this rank
+                                    // contributes are ready at kernel entry: one-kernel pull exchange)
   uint32_t wait_off;
   uint32_t signal_off;              // !=0: the last CTA to finish signals every rank with base + signal_off
   int32_t end_wait;                 // and then waits until every rank has signalled it

@@ -90,6 +90,10 @@ __device__ __forceinline__ Ep peer_enter(const PeerSync &s) {
   const Ep ep = peer_epochs(s);
   if (blockIdx.x == 0) trace_mark(s, 0);
   if (s.has_wait) {
+    if (s.entry_signal && threadIdx.x == 0) {   // every CTA (idempotent): no CTA waits on one not yet resident
+      __threadfence_system();
+      for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, ep.wait);
+    }
     peer_wait(s, ep.wait);
     if (blockIdx.x == 0) trace_mark(s, 1);
   }
@@ -214,7 +218,8 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
                nonfinite(vv[u].x) | nonfinite(vv[u].y) | nonfinite(vv[u].z) | nonfinite(vv[u].w);
         const int64_t q = q0 + u * stride;
         if (a.mc_w) {
-          mc_st4(a.mc_w + 4 * q, wv[u]);        // NVLS: every replica, this GPU's included
+          mc_st4(a.mc_w + 4 * q, wv[u]);        // NVLS: every replica, this GPU's included ...
+          st4(a.w + 4 * q, wv[u]);              // ... and the authoritative copy directly (later local reads)
         } else {
           st4(a.w + 4 * q, wv[u]);
           for (int b = 0; b < a.n_bcast; ++b)   // fused path: the updated slice goes straight to every replica
@@ -231,12 +236,10 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       float w = a.w[i], v = a.v[i];
       up(acc, w, v);
       bad |= nonfinite(w) | nonfinite(v);
-      if (a.mc_w) {
-        mc_st1(a.mc_w + i, w);
-      } else {
-        a.w[i] = w;
+      if (a.mc_w) mc_st1(a.mc_w + i, w);
+      a.w[i] = w;
+      if (!a.mc_w)
         for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
-      }
       a.v[i] = v;
     }
   } else {
@@ -246,12 +249,10 @@ __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_const
       float w = a.w[i], v = a.v[i];
       up(acc, w, v);
       bad |= nonfinite(w) | nonfinite(v);
-      if (a.mc_w) {
-        mc_st1(a.mc_w + i, w);
-      } else {
-        a.w[i] = w;
+      if (a.mc_w) mc_st1(a.mc_w + i, w);
+      a.w[i] = w;
+      if (!a.mc_w)
         for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][i] = w;
-      }
       a.v[i] = v;
     }
   }

@@ -112,15 +112,17 @@ struct ss_ctx {
   std::vector<const float *> win_bsp_src;      // gradients of the window's BSP events
   int32_t max_win = 16;
   // fused peer-memory path (G > 1): CUDA-IPC-mapped inboxes, replicas, pull buffers and flags
-  int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed
+  int32_t fused_mode = 1;              // 0 NCCL, 1 fused exact (ascending workers), 2 fused pre-summed, 3 fused pull
   bool ipc_ready = false;
   int64_t inbox_slots = 0;
   float *inbox = nullptr;              // [bufs][inbox_slots][reg_len] gradient slices owned here, written by peers
   int32_t inbox_bufs = 1;              // 2: exchanges alternate between two inbox buffers (no end barrier needed)
   int64_t xchg = 0;                    // fused exchanges issued (selects the inbox buffer)
   float *pbuf = nullptr;               // [n_hosted][P_pad] pull buffers of hosted workers, written by owners
+  float *gbuf = nullptr;               // [n_hosted][P_pad] gradient buffers of hosted workers, read by owners (mode 3)
   uint32_t *sigblk = nullptr;          // [0..7] inbound flags, [32] CTA counter, [64] timeout flag, [160] epoch counter
   float *peer_w[ss::kMaxPeers] = {}, *peer_inbox[ss::kMaxPeers] = {}, *peer_pbuf[ss::kMaxPeers] = {};
+  float *peer_gbuf[ss::kMaxPeers] = {};
   uint32_t *peer_sig[ss::kMaxPeers] = {};
   std::vector<void *> opened;          // peer mappings to close
   ss::NvlsReplica nvls;                // NVSwitch multicast replica (w lives here when ready)
@@ -405,8 +407,10 @@ void close_ipc(ss_ctx *c, bool all) {
   c->ipc_ready = false;
   if (all) {
     cudaFree(c->pbuf);
+    cudaFree(c->gbuf);
     cudaFree(c->sigblk);
     c->pbuf = nullptr;
+    c->gbuf = nullptr;
     c->sigblk = nullptr;
   }
 }
@@ -428,11 +432,14 @@ ss_status agree_all(ss_ctx *c, int32_t *flag) {
 ss_status ensure_nvls(ss_ctx *c) {
   if (c->nvls_tried) return SS_OK;
   c->nvls_tried = true;
-  // Default: on for world >= 8 only. Measured on this pool (tools/mc_bench.cu, profiles/r01_nvls_microbench.txt):
-  // at 4 GPUs a multicast store moves 181 GB/s of source data per GPU against 225 GB/s for P2P stores to all three
-  // peers; P2P is capped near 770/(G-1) GB/s of source, so multicast only wins from 8 GPUs on. SS_NVLS=0/1 overrides.
+  // Opt-in (SS_NVLS=1), off by default at every world size. Measured on this pool: at 4 GPUs a multicast store
+  // moves 181 GB/s of source data per GPU against 225 GB/s for P2P stores to all three peers
+  // (profiles/r01_nvls_microbench.txt), and the whole owner exchange — multimem.ld_reduce + multimem.st against P2P
+  // loads + P2P stores — reaches 76% vs 75% of 900 GB/s bus bandwidth at 4 GPUs and 40% vs 65% at 2
+  // (tools/nvls_reduce_bench.cu, profiles/r02_nvls_reduce_microbench.txt): no gain measured anywhere, so every world
+  // size runs the P2P code the 2- and 4-GPU tests cover.
   const char *env = getenv("SS_NVLS");
-  const bool want = env ? env[0] == '1' : c->world >= 8;
+  const bool want = env && env[0] == '1';
   int32_t ok = want && ss::nvls_supported(c->device) ? 1 : 0;
   SS_TRY(agree_all(c, &ok));
   if (!ok) return SS_OK;
@@ -482,6 +489,10 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   }
   c->inbox_bufs = two ? 2 : 1;
   if (!c->pbuf) SS_CUDA(c, cudaMalloc(&c->pbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+  if (!c->gbuf) {   // gradient buffers (mode 3): the padding stays zero, like every padded vector
+    SS_CUDA(c, cudaMalloc(&c->gbuf, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+    SS_CUDA(c, cudaMemset(c->gbuf, 0, (size_t)std::max(c->n_hosted, 1) * c->P_pad * sizeof(float)));
+  }
   if (!c->trace_dev && getenv("SS_TRACE") && getenv("SS_TRACE")[0]) {
     c->trace_path = getenv("SS_TRACE");
     const char *cap = getenv("SS_TRACE_CAP");
@@ -495,18 +506,20 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
   }
   c->inbox_slots = slots;
   SS_TRY(ensure_nvls(c));
-  cudaIpcMemHandle_t mine[4];
+  constexpr int kH = 5;   // exported buffers: w, inbox, pull buffers, flag block, gradient buffers
+  cudaIpcMemHandle_t mine[kH];
   std::memset(mine, 0, sizeof mine);
   if (!c->w_vmm) SS_CUDA(c, cudaIpcGetMemHandle(&mine[0], c->w));  // an NVLS replica is reached by multicast
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[1], c->inbox));
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[2], c->pbuf));
   SS_CUDA(c, cudaIpcGetMemHandle(&mine[3], c->sigblk));
+  SS_CUDA(c, cudaIpcGetMemHandle(&mine[4], c->gbuf));
   char *dev = nullptr;
   const size_t per = sizeof mine;
   SS_CUDA(c, cudaMalloc(&dev, per * c->world));
   SS_CUDA(c, cudaMemcpy(dev + per * c->rank, mine, per, cudaMemcpyHostToDevice));
   SS_NCCL(c, ncclAllGather(dev + per * c->rank, dev, per, ncclChar, c->comm, c->stream));
-  std::vector<cudaIpcMemHandle_t> all(4 * c->world);
+  std::vector<cudaIpcMemHandle_t> all(kH * c->world);
   SS_CUDA(c, cudaMemcpyAsync(all.data(), dev, per * c->world, cudaMemcpyDeviceToHost, c->stream));
   SS_CUDA(c, cudaStreamSynchronize(c->stream));
   cudaFree(dev);
@@ -516,17 +529,19 @@ ss_status ensure_fused(ss_ctx *c, int64_t slots) {
       c->peer_inbox[q] = c->inbox;
       c->peer_pbuf[q] = c->pbuf;
       c->peer_sig[q] = c->sigblk;
+      c->peer_gbuf[q] = c->gbuf;
       continue;
     }
-    void *p[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int k = c->w_vmm ? 1 : 0; k < 4; ++k) {
-      SS_CUDA(c, cudaIpcOpenMemHandle(&p[k], all[4 * q + k], cudaIpcMemLazyEnablePeerAccess));
+    void *p[kH] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    for (int k = c->w_vmm ? 1 : 0; k < kH; ++k) {
+      SS_CUDA(c, cudaIpcOpenMemHandle(&p[k], all[kH * q + k], cudaIpcMemLazyEnablePeerAccess));
       c->opened.push_back(p[k]);
     }
     c->peer_w[q] = (float *)p[0];
     c->peer_inbox[q] = (float *)p[1];
     c->peer_pbuf[q] = (float *)p[2];
     c->peer_sig[q] = (uint32_t *)p[3];
+    c->peer_gbuf[q] = (float *)p[4];
   }
   // every rank has mapped every peer before anyone signals through the mappings
   SS_NCCL(c, ncclAllGather(c->sigblk + 128 + c->rank, c->sigblk + 128, 1, ncclUint32, c->comm, c->stream));
@@ -571,7 +586,7 @@ int64_t inbox_off(const ss_ctx *c) {
 // when the inbox is single-buffered (the next phase A would overwrite slices still being read), or while capturing
 // (a graph replays its buffer choice, so keep the barrier).
 bool end_wait_needed(const ss_ctx *c, bool copy_follows) {
-  return copy_follows || c->inbox_bufs == 1 || c->capturing;
+  return copy_follows || c->inbox_bufs == 1 || c->capturing || c->nvls.ready;
 }
 
 // Phase A of every fused exchange: hosted sources' owner slices -> owners' inbox slots, then signal `epoch`.
@@ -717,7 +732,32 @@ ss_status flush(ss_ctx *c) {
   }
 
   if (cnt > 0) {
-    if (n_push == 0 && n_bsp_src == 0 && c->world == 1) {
+    if (c->world == 1 && c->win.size() == 1 && c->win[0].kind == 2) {
+      // a lone superstep (flushed at its data dependency): the streaming aggregate-and-update kernel, which reads
+      // each gradient once and w, v once — the same arithmetic as the window kernel's BSP event
+      const Ev &e = c->win[0];
+      ss::BspArgs a;
+      std::memset(&a, 0, sizeof a);
+      bool vec = aligned16(c->w) && aligned16(c->v);
+      for (int32_t k = 0; k < e.n_src; ++k) {
+        a.g[k] = c->win_bsp_src[e.src0 + k];
+        vec = vec && aligned16(a.g[k]);
+      }
+      a.n_in = e.n_src;
+      a.flag = c->flag;
+      a.divisor = e.divisor;
+      a.mu = e.mu;
+      a.neg_eta = -e.lr;
+      a.lam = c->lam;
+      a.nesterov = c->nesterov;
+      a.w = c->w;
+      a.v = c->v;
+      a.count = c->P;
+      Timed t;
+      timed_begin(c, &t, 0, 4.0 * (double)c->P * (e.n_src + 4));
+      SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
+      timed_end(c, &t);
+    } else if (n_push == 0 && n_bsp_src == 0 && c->world == 1) {
       // pulls only: plain copies of the current w
       for (const Ev &e : c->win)
         if (e.data) SS_CUDA(c, cudaMemcpyAsync(e.dst, c->w, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -1163,11 +1203,12 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   bool vec = true;
   int32_t k = 0;
   std::vector<int32_t> ids;             // hosted members, ascending
+  const bool pull = c->world > 1 && c->fused_mode == 3;
   for (int32_t j = 0; j < c->n; ++j) {  // ascending worker order (reading C12)
     if (!by[j]) continue;
     ids.push_back(j);
-    const float *g = nullptr;
-    SS_TRY(resolve_src(c, by[j], &g));
+    const float *g = by[j];
+    if (!pull) SS_TRY(resolve_src(c, by[j], &g));   // (pull mode copies straight into its gradient buffers)
     a.g[k++] = g;
     vec = vec && aligned16(g);
   }
@@ -1187,6 +1228,80 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
+  } else if (pull) {
+    // Fused pull exchange (SURVEY §8(f) NEXT-1 as one kernel, "push the computed gradients to all PSs"): every
+    // rank's hosted gradients sit in its exported gradient buffers (ss_grad_buffer hands them out: zero copy; any other
+    // buffer is copied in on the stream first). Each owner loads the members' slices of its region — hosted ones from
+    // local HBM, the others from the peers' buffers over NVLink — sums them in ascending worker order (bit-identical to
+    // one GPU), updates w and v, and stores the new slice into every replica. Cross-GPU barriers: at entry (every rank
+    // signals that its gradients are in place, then waits for all) and at exit (no rank reuses a gradient buffer or
+    // reads its replica before every owner is done).
+    SS_TRY(ensure_fused(c, c->max_win));
+    const int32_t me = c->rank;
+    const int64_t lo = c->real_lo[me], cnt = c->real_hi[me] - lo;
+    for (int32_t i = 0; i < k; ++i) {
+      float *dst = c->gbuf + (int64_t)(ids[i] - c->first_hosted) * c->P_pad;
+      if (a.g[i] != dst)
+        SS_CUDA(c, cudaMemcpyAsync(dst, a.g[i], (size_t)c->P * sizeof(float), cudaMemcpyDefault, c->stream));
+    }
+    std::memset(a.g, 0, sizeof a.g);
+    int32_t ni = 0, remote = 0;
+    for (int32_t j = 0; j < c->n; ++j) {   // the members' slices, ascending worker order
+      if (!c->member[j]) continue;
+      const int32_t h = host_of(c, j);
+      a.g[ni++] = c->peer_gbuf[h] + (int64_t)(j - first_hosted_of(c, h)) * c->P_pad + lo;
+      remote += h != me;
+    }
+    a.n_in = ni;
+    a.w = c->w + lo;
+    a.v = c->v;
+    a.count = cnt;
+    a.n_bcast = 0;
+    if (c->nvls.ready) {
+      a.mc_w = (float *)c->nvls.mcv + lo;
+    } else {
+      for (int32_t step = 1; step < c->world; ++step)   // rotated: the ranks' stores go to distinct receivers
+        a.bcast[a.n_bcast++] = c->peer_w[(me + step) % c->world] + lo;
+    }
+    const uint32_t epA = ++c->epoch, epB = ++c->epoch;
+    a.sync = peer_sync(c, epA, epB, true, 2);
+    a.sync.entry_signal = 1;
+    Timed t;
+    // NVLink bytes per direction: the remote slices this owner loads (the peers load as many of this rank's
+    // gradients) plus the slices it stores into the other replicas (as many arrive from the other owners)
+    timed_begin(c, &t, 0, 4.0 * (double)cnt * (ni + 4), 4.0 * (double)cnt * (remote + (c->world - 1)));
+    if (!c->nvls.ready && ni <= ss::kMaxBspSrc) {
+      // the window kernel's form (measured 0.717 vs 0.689 of 900 GB/s bus bandwidth for the register form at 4 GPUs,
+      // config 5a): one BSP event whose sources — the local and peer gradient slices — are staged by 1-D bulk copies
+      // (the TMA engine reads the peers' memory over NVLink), then one store event per peer replica
+      ss::AspArgs r;
+      std::memset(&r, 0, sizeof r);
+      ss::AspEvent &x = r.ev[0];
+      x.kind = 2;
+      x.lr = -a.neg_eta;
+      x.mu = a.mu;
+      x.divisor = a.divisor;
+      x.src0 = 0;
+      x.n_src = ni;
+      for (int32_t i = 0; i < ni; ++i) r.bsp_src[i] = a.g[i];
+      for (int32_t b = 0; b < a.n_bcast; ++b) {
+        r.ev[1 + b].kind = 1;
+        r.ev[1 + b].dst = a.bcast[b];
+      }
+      r.n_ev = 1 + a.n_bcast;
+      r.w = a.w;
+      r.v = a.v;
+      r.flag = a.flag;
+      r.count = cnt;
+      r.lam = a.lam;
+      r.nesterov = a.nesterov;
+      r.sync = a.sync;
+      SS_CUDA(c, ss::launch_asp_replay(r, true, c->stream));
+    } else {
+      SS_CUDA(c, ss::launch_bsp_update(a, true, c->stream));   // NVLS (opt-in) multicast stores; > 128 members
+    }
+    timed_end(c, &t);
+    c->xchg += 1;
   } else if (c->fused_mode != 0) {
     // Fused peer-memory BSP. Phase A: scatter hosted gradients (exact mode) or this rank's
     // pre-sum (mode 2) into the owners' inboxes. Phase B: owner sums its inbox slots in ascending order, updates
@@ -1528,7 +1643,7 @@ ss_status ss_set_window(ss_ctx *c, int32_t max_events) {
 
 ss_status ss_set_fused(ss_ctx *c, int32_t mode) {
   SS_TRY(check_live(c));
-  if (mode < 0 || mode > 2) return fail(c, SS_E_INVAL, "fused mode must be 0, 1 or 2");
+  if (mode < 0 || mode > 3) return fail(c, SS_E_INVAL, "fused mode must be 0, 1, 2 or 3");
   SS_TRY(flush(c));
   c->fused_mode = mode;
   return SS_OK;
@@ -1548,6 +1663,16 @@ ss_status ss_pull_buffer(ss_ctx *c, int32_t worker, float **out) {
   if (host_of(c, worker) != c->rank) return fail(c, SS_E_INVAL, "worker %d is not hosted on this rank", worker);
   SS_TRY(ensure_fused(c, c->max_win));
   *out = c->pbuf + (int64_t)(worker - c->first_hosted) * c->P_pad;
+  return SS_OK;
+}
+
+ss_status ss_grad_buffer(ss_ctx *c, int32_t worker, float **out) {
+  SS_TRY(check_live(c));
+  if (!out || worker < 0 || worker >= c->n) return fail(c, SS_E_INVAL, "bad worker or null output");
+  if (c->world == 1 || c->fused_mode == 0) return fail(c, SS_E_STATE, "gradient buffers exist in fused multi-GPU mode");
+  if (host_of(c, worker) != c->rank) return fail(c, SS_E_INVAL, "worker %d is not hosted on this rank", worker);
+  SS_TRY(ensure_fused(c, c->max_win));
+  *out = c->gbuf + (int64_t)(worker - c->first_hosted) * c->P_pad;
   return SS_OK;
 }
 

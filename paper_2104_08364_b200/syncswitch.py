@@ -30,7 +30,7 @@ EXPORTS = ["ss_init", "ss_init_dist", "ss_nccl_unique_id", "ss_destroy", "ss_las
            "ss_asp_replay", "ss_sync", "ss_flush", "ss_read_params", "ss_read_velocity", "ss_get_stats", "ss_get_log",
            "ss_set_window", "ss_get_stream", "ss_wait_stream", "ss_profile", "ss_kernel_stats", "ss_synth_grad",
            "ss_softmax_grad", "ss_table1", "ss_schedule", "ss_detector_new", "ss_detector_window",
-           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_set_nesterov", "ss_get_exchange", "ss_pull_buffer",
+           "ss_detector_free", "ss_greedy_decision", "ss_route_plan", "ss_set_fused", "ss_set_nesterov", "ss_get_exchange", "ss_pull_buffer", "ss_grad_buffer",
            "ss_scenario_run", "ss_set_momentum_policy", "ss_set_members", "ss_detector_window_masked",
            "ss_dynamic_criterion", "ss_criterion_observe", "ss_capture_begin", "ss_capture_end",
            "ss_capture_replay"]
@@ -87,6 +87,7 @@ def _load():
         "ss_get_exchange": [p, p, p],
         "ss_set_nesterov": [p, i32],
         "ss_pull_buffer": [p, i32, p],
+        "ss_grad_buffer": [p, i32, p],
         "ss_nccl_unique_id": [p],
         "ss_set_lr_schedule": [p, p, p, i32],
         "ss_set_lr_policy": [p, i32, f32],
@@ -457,6 +458,12 @@ class SyncSwitch:
     def pull_buffer(self, worker: int) -> int:
         out = ctypes.c_void_p()
         self._chk(lib.ss_pull_buffer(self.ctx, worker, ctypes.byref(out)))
+        return out.value
+
+    def grad_buffer(self, worker: int) -> int:
+        """Address of the exported gradient buffer of a hosted worker (fused mode 3 reads it in place)."""
+        out = ctypes.c_void_p()
+        self._chk(lib.ss_grad_buffer(self.ctx, worker, ctypes.byref(out)))
         return out.value
 
     def set_lr_schedule(self, boundaries, factors):

@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--pushes", type=int, default=60)
     ap.add_argument("--bsp2", type=int, default=2)
     ap.add_argument("--fused", type=int, default=-1)
+    ap.add_argument("--gbuf", type=int, default=0,
+                    help="superstep gradients written into the context's exported gradient buffers (zero copy)")
     ap.add_argument("--drop", type=int, default=-1, help="elastic: worker left out of --bsp-drop BSP steps")
     ap.add_argument("--bsp-drop", type=int, default=0)
     ap.add_argument("--sample", type=int, default=0, help="save only this many sampled elements (full-size runs)")
@@ -85,6 +87,24 @@ def main():
         keep.append(buf)
         return buf
 
+    def bsp_grads(ids):
+        """Gradients of one superstep. --gbuf: written in place into ss_grad_buffer (the previous superstep borrowed
+        them until ss_sync, so sync first; synth_grad runs on the library's stream behind it)."""
+        if not a.gbuf:
+            return {j: grad(j) for j in ids}
+        g.sync()
+        out = {}
+        for j in ids:
+            k = counter[j]
+            counter[j] += 1
+            if j in hosted:
+                ptr = g.grad_buffer(j)
+                ss.ss_check(ss.ss_synth_grad(SEED, j, k, 0, P, ptr, g.stream))
+                out[j] = ptr
+            else:
+                out[j] = None
+        return out
+
     if a.scenario >= 0:
         sc = dict(n_workers=n, batch=128, total_samples=600 * 128, quota_num=1, quota_den=2, period=1000, jitter=0,
                   sched_seed=7, grad_seed=SEED, slow_worker=n - 1, slow_factor=4, slow_t0=3000, slow_t1=30000,
@@ -132,7 +152,7 @@ def main():
         return
 
     for _ in range(a.bsp1):
-        gs = {j: grad(j) for j in range(n)}
+        gs = bsp_grads(range(n))
         g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
     if a.nan_bsp:
         gs = {j: grad(j) for j in range(n)}
@@ -171,7 +191,7 @@ def main():
             stale.append(g.asp_push(j, grad(j), base[j]))
     g.switch(ss.SS_BSP, 0)
     for _ in range(a.bsp2):
-        gs = {j: grad(j) for j in range(n)}
+        gs = bsp_grads(range(n))
         g.bsp_step([gs[j] for j in hosted], hosted, [g.version] * len(hosted))
     g.sync()
     w = g.params()

@@ -31,7 +31,7 @@ class Program:
         self.nesterov = bool(rng.integers(0, 4) == 0)
         self.bounds = sorted(int(b) for b in rng.choice(np.arange(1, 60), size=2, replace=False))
         self.factors = [0.1, 0.01]
-        self.fused = int(rng.integers(0, 3)) if world > 1 else -1
+        self.fused = int(rng.integers(0, 4)) if world > 1 else -1
         self.n_ops = int(rng.integers(20, 80))
 
     def next_op(self, protocol: int, version: int, base: dict):

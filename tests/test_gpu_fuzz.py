@@ -174,7 +174,7 @@ def check_multi(orc, prog: Program, ranks):
     """Every rank's records (dist_fuzz_worker.py) against the oracle's run of the same program."""
     o, rec_o, snaps_o, is_bsp = run_oracle(orc, prog)
     # bit-exact unless a BSP superstep was applied with another summation order (NCCL or pre-summed mode)
-    exact = prog.fused == 1 or not np.any(rec_o[is_bsp, 0] == 0)
+    exact = prog.fused in (1, 3) or not np.any(rec_o[is_bsp, 0] == 0)
     same = np.array_equal if exact else close_c13
     st = o.stats(64)
     for q, d in enumerate(ranks):

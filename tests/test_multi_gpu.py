@@ -82,22 +82,25 @@ def close_c13(x, y, rel=1e-5):
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", ["asp_only", "switched", "switched_fused", "switched_presum", "elastic_fused",
-                                  "elastic_nccl", "nesterov_fused"])
+                                  "elastic_nccl", "nesterov_fused", "switched_pull", "switched_pull_gbuf",
+                                  "elastic_pull"])
 def test_multi_gpu_parity(orc, world, case):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     P, n, S, win = 100003, 8, 8, 7
     bsp1, pushes, bsp2 = (0, 80, 0) if case == "asp_only" else (3, 60, 2)
-    fused = {"switched_fused": 1, "switched_presum": 2, "elastic_fused": 1, "nesterov_fused": 1}.get(case, 0)
+    fused = {"switched_fused": 1, "switched_presum": 2, "elastic_fused": 1, "nesterov_fused": 1, "switched_pull": 3,
+             "switched_pull_gbuf": 3, "elastic_pull": 3}.get(case, 0)
+    gbuf = int(case.endswith("gbuf"))       # mode 3 with the gradients written into ss_grad_buffer (zero copy)
     nest = case.startswith("nesterov")
     drop, bsp_drop = (1, 3) if case.startswith("elastic") else (-1, 0)
     with tempfile.TemporaryDirectory() as tmp:
         launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", win, "--bsp1", bsp1, "--pushes", pushes,
-                       "--bsp2", bsp2, "--fused", fused, "--drop", drop, "--bsp-drop", bsp_drop, "--nesterov", int(nest)],
-               tmp)
+                       "--bsp2", bsp2, "--fused", fused, "--drop", drop, "--bsp-drop", bsp_drop, "--nesterov", int(nest),
+                       "--gbuf", gbuf], tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, bsp1, pushes, bsp2, drop, bsp_drop, nesterov=nest)
-    exact = case in ("asp_only", "switched_fused", "elastic_fused", "nesterov_fused")   # NCCL / pre-summed: other sum orders (C13)
+    exact = fused in (1, 3) or case == "asp_only"   # NCCL / pre-summed: other summation orders (C13)
     ow, ov = o.params(), o.velocity()
     for q, r in enumerate(res):
         # worker placement: the oracle's worker -> GPU map (a1)
@@ -127,12 +130,12 @@ def test_multi_gpu_parity(orc, world, case):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fused,nvls", [(1, 0), (2, 0), (1, 1), (2, 1)])
+@pytest.mark.parametrize("fused,nvls", [(1, 0), (2, 0), (3, 0), (1, 1), (2, 1)])
 def test_multi_gpu_full_size_sampled(orc, world, fused, nvls):
     """Config 3 at full size (P = 25,557,032, n = S = 8, window 16: the bench's configuration) on `world` GPUs:
     1 BSP superstep, a switch, 16 seeded ASP pushes with pulls, a switch back and 1 BSP superstep; 4,096 sampled
     elements against the oracle (bit-exact in fused-exact mode, C13 in pre-summed mode), integers exact. nvls = 1
-    forces the NVSwitch-multicast broadcast (SS_NVLS=1), the default branch from 8 GPUs on."""
+    forces the opt-in NVSwitch-multicast broadcast (SS_NVLS=1)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -140,13 +143,14 @@ def test_multi_gpu_full_size_sampled(orc, world, fused, nvls):
     P, n, S = 25_557_032, 8, 8
     with tempfile.TemporaryDirectory() as tmp:
         launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 16, "--bsp1", 1, "--pushes", 16,
-                       "--bsp2", 1, "--fused", fused, "--sample", 4096], tmp, env={"SS_NVLS": str(nvls)})
+                       "--bsp2", 1, "--fused", fused, "--sample", 4096, "--gbuf", int(fused == 3)], tmp,
+               env={"SS_NVLS": str(nvls)})
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
     if nvls and not all(int(r["nvls"]) for r in res):
         pytest.skip("NVLS multicast unavailable on this box")
     idx = sample_indices(P, 4096)
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 1, 16, 1, idx=idx)
-    exact = fused == 1
+    exact = fused in (1, 3)
     for r in res:
         assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
         cmp = np.array_equal if exact else close_c13
@@ -164,7 +168,7 @@ def test_multi_gpu_full_size_sampled(orc, world, fused, nvls):
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("shape", [(33, 3, 4), (1003, 6, 4), (97, 1, 4), (4099, 5, 8)])
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 def test_multi_gpu_edge_layouts(orc, world, shape, fused):
     """Layouts the bench never uses: ranks hosting no worker (n < G), owner regions past the end of a tiny vector
     (P = 33 on 4 ranks of 32-float shards), one worker for the whole job, n not a multiple of G; every exchange mode.
@@ -179,7 +183,7 @@ def test_multi_gpu_edge_layouts(orc, world, shape, fused):
                        "--bsp2", 2, "--fused", fused], tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 2, 24, 2)
-    cmp = np.array_equal if fused == 1 else close_c13
+    cmp = np.array_equal if fused in (1, 3) else close_c13
     for r in res:
         assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
         assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
@@ -198,7 +202,7 @@ def test_multi_gpu_edge_layouts(orc, world, shape, fused):
 @pytest.mark.parametrize("fused", [1, 2])
 @pytest.mark.parametrize("P", [100003, 33])
 def test_multi_gpu_nvls_forced(orc, world, fused, P):
-    """The NVSwitch-multicast broadcast (default from 8 GPUs) forced on at 2 and 4 GPUs (SS_NVLS=1): BSP supersteps
+    """The opt-in NVSwitch-multicast broadcast forced on at 2 and 4 GPUs (SS_NVLS=1): BSP supersteps
     store each updated slice once through the multicast view. Same results as the P2P broadcast: bit-exact in
     fused-exact mode, C13 in pre-summed mode. Skipped when the driver / fabric offers no multicast."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
@@ -211,7 +215,7 @@ def test_multi_gpu_nvls_forced(orc, world, fused, P):
     if not all(int(r["nvls"]) for r in res):
         pytest.skip("NVLS multicast unavailable on this box")
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 3, 40, 3)
-    cmp = np.array_equal if fused == 1 else close_c13
+    cmp = np.array_equal if fused in (1, 3) else close_c13
     for r in res:
         assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
         assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
@@ -227,7 +231,7 @@ def test_multi_gpu_nvls_forced(orc, world, fused, P):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 def test_multi_gpu_graph_capture(orc, world, fused):
     """ss_capture_* at G > 1 (SURVEY §8(d) config 2 "with and without CUDA Graphs"): the bench step captured once and
     replayed 6 times on every rank equals 8 ordinary steps of the oracle — the fused kernels' flag epochs come from a
@@ -253,7 +257,7 @@ def test_multi_gpu_graph_capture(orc, world, fused):
             assert o.asp_push(j, asp_h[j], v + 1) == (0, j)
             snaps[j] = o.pull(j)[1]
         o.switch(orc.BSP, 0)
-    cmp = np.array_equal if fused == 1 else close_c13
+    cmp = np.array_equal if fused in (1, 3) else close_c13
     for r in res:
         assert int(r["version"]) == o.version == (R + 2) * (1 + n)
         assert np.array_equal(r["log"], o.log()) and np.array_equal(r["hist"], o.stats(64)["hist"])
@@ -263,7 +267,7 @@ def test_multi_gpu_graph_capture(orc, world, fused):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fused", [0, 1])
+@pytest.mark.parametrize("fused", [0, 1, 3])
 def test_multi_gpu_host_buffers(orc, world, fused):
     """The e2e path at G > 1: gradients and pull destinations in pinned host memory (staged by the library) —
     same results as device buffers (bit-exact in fused-exact mode)."""
@@ -275,7 +279,7 @@ def test_multi_gpu_host_buffers(orc, world, fused):
                        "--bsp2", 1, "--fused", fused, "--host-buffers", 1], tmp)
         res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
     o, stale, snaps, kind, worker = oracle_run(orc, P, n, S, 2, 30, 1)
-    cmp = np.array_equal if fused == 1 else close_c13
+    cmp = np.array_equal if fused in (1, 3) else close_c13
     for r in res:
         assert list(r["stale"]) == stale and np.array_equal(r["log"], o.log())
         assert cmp(r["w"], o.params())
