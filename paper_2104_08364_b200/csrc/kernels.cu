@@ -31,6 +31,13 @@ constexpr int kThreads = 256;
 __device__ __forceinline__ float4 ld4(const float *p) { return __ldcg(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ void st4(float *p, float4 x) { __stcs(reinterpret_cast<float4 *>(p), x); }
 
+// Programmatic dependent launch (the streaming kernels are launched with programmatic stream serialization): a
+// kernel lets the next one on the stream be scheduled as soon as all of its CTAs are resident (trigger), and reads
+// nothing another kernel wrote before griddepcontrol.wait returns — which is when the previous grid has completed and
+// its memory operations are visible. The next launch's scheduling and prologue then overlap this kernel's tail.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------------------------------------------
 // Cross-GPU flag barrier (fused path). Release/acquire at system scope over NVLink-mapped peer memory; every wait
 // is bounded (kTimeoutNs) so a missing peer can never hang the GPU: the wait gives up and raises *err.
@@ -174,6 +181,8 @@ constexpr int kG1 = SS_BSP_G;  // gradients loaded together
 // launch smaller than one wave of it uses <1, 4>: profiles/r01_bsp_sweep.txt, config 2)
 template <bool VEC, int U = kU1, int GL = kG1>
 __global__ void __launch_bounds__(kThreads) bsp_update_kernel(const __grid_constant__ BspArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const Ep ep = peer_enter(a.sync);
   const Upd up{a.divisor, 1.0f / a.divisor, a.mu, a.neg_eta, a.lam, is_pow2(a.divisor), a.nesterov != 0};
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -400,7 +409,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // into a register accumulator, then the mean and the momentum update), pull (store of the current w).
 template <bool kRefill>
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
-  const Ep ep = peer_enter(a.sync);
+  pdl_trigger();
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ const float *item_src[kMaxItems];
@@ -432,9 +441,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
       }
     }
   };
-  if (my_tiles > 0) load_wv(0);
-
-  // Prologue, warp 0: list the gradient sources of a tile in event order (lane l takes events l and l + 32; their
+  // Prologue, warp 0 (kernel parameters and shared memory only, so it overlaps the previous kernel's tail): list the gradient sources of a tile in event order (lane l takes events l and l + 32; their
   // item offsets are a warp prefix sum of the per-event source counts) and initialise the ring's barriers.
   static_assert(kMaxEvents <= 64, "two events per lane");
   if (threadIdx.x < 32) {
@@ -460,11 +467,14 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     list(lane, s0 - c0, c0);
     list(lane + 32, tot0 + s1 - c1, c1);
     for (int st = lane; st < n_stage; st += 32) mbar_init(&full[st], 1);
-    // the bulk copies below (async proxy) may read inbox slices peers wrote before the flag this CTA acquired
-    // (generic proxy): order them after the acquire
-    if (a.sync.has_wait) asm volatile("fence.proxy.async.global;" ::: "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();                                                // from here on: data of earlier kernels
+  const Ep ep = peer_enter(a.sync);
+  // the bulk copies below (async proxy) may read slices peers wrote before the flag this CTA acquired (generic
+  // proxy): order them after the acquire
+  if (a.sync.has_wait && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (my_tiles > 0) load_wv(0);
   __syncthreads();
 
   // Items are staged and consumed in order, so both sides walk cursors instead of dividing by the runtime ring depth
@@ -911,6 +921,23 @@ int grid_for(K kernel, int64_t work_items) {
 
 }  // namespace
 
+// Launch with programmatic stream serialization (see pdl_trigger / pdl_wait): only kernels that call pdl_wait before
+// touching global data written by earlier work are launched this way.
+template <typename Arg>
+cudaError_t launch_pdl(void (*k)(Arg), int64_t grid, size_t smem, cudaStream_t s, const Arg &arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, arg);
+}
+
 cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
   if (a.count <= 0 && !a.sync.has_wait && a.sync.signal_off == 0) return cudaSuccess;
   if (vec) {
@@ -919,15 +946,12 @@ cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
     if (n4 < (int64_t)resident_ctas(k) * num_sms() * kThreads * kU1) {
       // less than one wave of the streaming form (small P, e.g. config 2): latency-bound, one float4 per thread
       auto ks = bsp_update_kernel<true, 1, 4>;
-      ks<<<grid_for(ks, n4 + 1), kThreads, 0, s>>>(a);
-    } else {
-      k<<<grid_for(k, (n4 + kU1 - 1) / kU1 + 1), kThreads, 0, s>>>(a);
+      return launch_pdl(ks, grid_for(ks, n4 + 1), 0, s, a);
     }
-  } else {
-    auto k = bsp_update_kernel<false>;
-    k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
+    return launch_pdl(k, grid_for(k, (n4 + kU1 - 1) / kU1 + 1), 0, s, a);
   }
-  return cudaGetLastError();
+  auto k = bsp_update_kernel<false>;
+  return launch_pdl(k, grid_for(k, a.count), 0, s, a);
 }
 
 cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
@@ -974,8 +998,7 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
       b.tile = (int32_t)t;
       b.stages = b.n_item;
       const int64_t grid = std::max<int64_t>(1, (nvec + t - 1) / t);
-      asp_replay_tma_kernel<false><<<(int)grid, kThreads, (size_t)smem, s>>>(b);
-      return cudaGetLastError();
+      return launch_pdl(asp_replay_tma_kernel<false>, grid, (size_t)smem, s, b);
     }
   }
   // streaming form: grid-stride over kTmaTile tiles, at most one wave of resident CTAs, a kTmaStages-tile ring
@@ -986,11 +1009,8 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   b.tile = (int32_t)tile;
   b.stages = kTmaStages;
   const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
-  if (items > kTmaStages)
-    asp_replay_tma_kernel<true><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
-  else
-    asp_replay_tma_kernel<false><<<(int)grid, kThreads, kTmaSmem, s>>>(b);
-  return cudaGetLastError();
+  if (items > kTmaStages) return launch_pdl(asp_replay_tma_kernel<true>, grid, kTmaSmem, s, b);
+  return launch_pdl(asp_replay_tma_kernel<false>, grid, kTmaSmem, s, b);
 }
 
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {

@@ -321,7 +321,7 @@ def test_multi_gpu_scenario(orc, world, policy):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 def test_multi_gpu_divergence_reaches_every_rank(orc, world, fused):
     """A non-finite gradient element owned by the last rank: only that rank's kernels see the non-finite update, but
     ss_sync is collective and agrees on the divergence flag, so EVERY rank returns SS_E_DIVERGED at the same ss_sync
