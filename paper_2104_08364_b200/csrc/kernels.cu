@@ -622,6 +622,8 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
 // scatter (fused path): every hosted gradient's owner slices go to the owners' inboxes with
 // posted 128-bit NVLink stores (the local slice is read in place by the owner update, never copied).
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const Ep ep = peer_enter(a.sync);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -659,6 +661,8 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 // after another left the own region's HBM pass on the critical path after the NVLink-bound ones).
 constexpr int kScsU = 2;   // float4 chunks per thread per iteration
 __global__ void __launch_bounds__(kThreads) scatter_sum_kernel(const __grid_constant__ ScatterArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const Ep ep = peer_enter(a.sync);
   const int me = a.sync.rank, G = a.sync.world;
   // interleave cycle of G CTAs: CTA k of each cycle serves region (me + 1 + k) % G (k = G - 1: the own region);
@@ -1017,15 +1021,13 @@ cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
   const int G = a.sync.world > 0 ? a.sync.world : 1;
   const int grid = (std::max(grid_for(k, (a.P / 4 + kScsU - 1) / kScsU + 1), G) + G - 1) / G * G;   // whole cycles
-  k<<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, 0, s, a);
 }
 
 cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_kernel;
   const int64_t work = a.n_src > 0 ? (a.P / 4 + 3) / 4 + 1 : 1;
-  k<<<grid_for(k, work), kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid_for(k, work), 0, s, a);
 }
 
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
