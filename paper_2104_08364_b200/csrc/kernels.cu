@@ -991,8 +991,7 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   // Small-launch form: one tile per CTA, every gradient source of it staged at once (no stage reuse, no CTA
   // barrier per item), as many CTAs as fit (up to 4 per SM at 64 registers x 256 threads); tiles are a multiple of
   // 32 floats (128 B). Used when such a tile is no longer than the streaming form's.
-  static const bool small_form = !(getenv("SS_REPLAY_STREAMING") && getenv("SS_REPLAY_STREAMING")[0] == '1');
-  if (small_form && b.n_item > 0 && b.n_item <= kMaxStages) {
+  if (b.n_item > 0 && b.n_item <= kMaxStages) {   // (config 2, 1 GPU: 61.6k vs 60.8k steps/s streaming-only)
     for (int per_sm = 4; per_sm >= 1; --per_sm) {
       const int64_t want = (int64_t)per_sm * num_sms();
       const int64_t t = std::max<int64_t>(32, ((nvec + want - 1) / want + 31) / 32 * 32);
