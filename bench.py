@@ -489,8 +489,7 @@ def run_ours(args):
                   "bsp_ms_per_step": bsp_ms / args.steps, "asp_ms_per_round": asp_ms / args.steps,
                   "profiled_ms_per_step": prof_ms / args.steps,
                   "note": "from the profiled pass (events at every launch and phase boundary); one GPU: the superstep "
-                          "runs in the window kernel (bsp_window: a window holding one BSP event), the ASP round in "
-                          "asp_replay"}
+                          "runs in bsp_update, the ASP round in the window kernel asp_replay"}
     else:
         phases = {"bsp_steps_per_s": args.steps / (bsp_ms / 1e3), "asp_pushes_per_s": n * args.steps / (asp_ms / 1e3),
                   "bsp_ms_per_step": bsp_ms / args.steps, "asp_ms_per_round": asp_ms / args.steps,
@@ -505,6 +504,19 @@ def run_ours(args):
         phases["bsp_nvlink_frac_of_770_measured"] = phases["bsp_nvlink_busbw_GBps"] / 770.0
         rates["bsp_nvlink_busbw_GBps"] = per_dir / (bsp_only_ms / nr / 1e3) / 1e9
         rates["bsp_nvlink_frac_of_900"] = rates["bsp_nvlink_busbw_GBps"] / 900.0
+    # the step's floor on this N: the bytes the method must move through the bounding link, at its peak.
+    # G > 1: per GPU per direction, the BSP exchange (RS + AG: 2(G-1)/G * 4 P_pad) plus the ASP round (n pushes routed
+    # to the owners and n pull snapshots routed back, n/G of each per GPU: 2 (n/G)(G-1)/G * 4 P_pad), over 900 GB/s
+    # NVLink; G = 1: the two kernels' HBM bytes over the measured copy rate.
+    if world > 1:
+        P_pad = S * (((P + S - 1) // S + 31) // 32 * 32)
+        nv_bytes = 2 * (world - 1) / world * 4 * P_pad * (1 + n / world)
+        floor = {"bound": "nvlink", "bytes_per_gpu_per_direction": nv_bytes, "peak_GBps": 900.0,
+                 "steps_per_s_at_peak": 900e9 / nv_bytes}
+    else:
+        floor = {"bound": "hbm", "bytes": step_bytes, "peak_GBps": hbm_peak,
+                 "steps_per_s_at_peak": hbm_peak * 1e9 / step_bytes}
+    floor["frac_of_floor"] = steps_per_s / floor["steps_per_s_at_peak"]
     line = {
         "metric": METRIC, "value": round(steps_per_s, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -520,7 +532,7 @@ def run_ours(args):
                           f"inputs larger than L2: gradients rotate over {R} sets ({R * set_bytes / 1e6:.0f} MB per "
                           f"rank, >= 3x the 126 MB L2), no flush; PS state w, v ({8 * P / world / 1e6:.1f} MB) and "
                           f"pull buffers stay resident")},
-        "phases": phases, "protocol_rates": rates, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
+        "phases": phases, "protocol_rates": rates, "step_floor": floor, "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clk,
         "graph": graph,
         "e2e": e2e,
         "protocol_check": {"version": st["version"], "hist_0_to_n": [int(x) for x in st["hist"][:n + 1]]},

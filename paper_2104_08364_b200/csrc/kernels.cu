@@ -938,7 +938,11 @@ cudaError_t launch_pdl(void (*k)(Arg), int64_t grid, size_t smem, cudaStream_t s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
+#ifdef SS_NO_PDL
+  cfg.numAttrs = 0;   // A/B variant (tools/kernel_sweep.py set "pdl"): ordinary stream serialisation
+#else
   cfg.numAttrs = 1;
+#endif
   return cudaLaunchKernelEx(&cfg, k, arg);
 }
 

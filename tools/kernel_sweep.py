@@ -17,6 +17,7 @@ SETS = {
                [(2048, 6), (2048, 10), (2048, 12), (2048, 14), (2048, 16), (1024, 20), (4096, 6)]],
     "balance": [{"SS_TMA_BALANCE": b, "SS_TMA_STAGES": st} for b, st in [(0, 10), (1, 10), (0, 12), (1, 12)]],
     "bsp": [{"SS_BSP_U": u, "SS_BSP_G": g} for u, g in [(2, 8), (1, 8), (1, 4), (2, 4), (4, 4), (4, 2), (3, 8)]],
+    "pdl": [{"SS_NO_PDL": 1}],   # programmatic dependent launch off (A/B against the default library)
 }
 
 
