@@ -40,7 +40,10 @@ def _setup(ss, orc, P, n, S):
     g = ss.SyncSwitch(torch.from_numpy(w0).cuda(), S, n, 0.1, 0.9)
     o = orc.Oracle(w0, S, n, 0.1, 0.9)
     gb = [orc.synth_grad(SEED, j, 0, 0, P) for j in range(n)]
-    g.bsp_step([torch.from_numpy(x).cuda() for x in gb])
+    dg = [torch.from_numpy(x).cuda() for x in gb]
+    g.bsp_step(dg)
+    g.flush()                                               # issue the (deferred) superstep while dg is alive
+    g.sync()
     assert o.bsp_step(gb) == 0
     g.switch(ASP, 0)
     o.switch(ASP, 0)
@@ -130,4 +133,32 @@ def test_rejected_push_under_bsp_counts_drop_only(ss, orc):
     assert (v1, d1) == (v0, d0 + 1) and np.array_equal(h0, h1) and np.array_equal(l0, l1)
     assert o.asp_push(0, orc.synth_grad(SEED, 0, 1, 0, P), 1)[0] == SS_E_STATE
     assert o.stats()["dropped"] == d1
+    g.close()
+
+
+def test_flush_and_grad_buffer_contract(ss, orc):
+    """ss_flush issues pending work without changing protocol state and is a no-op on an empty window; it returns
+    SS_E_DIVERGED (sticky) once a non-finite value was produced. ss_grad_buffer exists only in fused multi-GPU mode:
+    SS_E_STATE on one GPU, SS_E_INVAL for a bad worker or null output."""
+    P, n, S = 1000, 2, 2
+    g, o = _setup(ss, orc, P, n, S)
+    before = _state(g)
+    assert ss.lib.ss_flush(g.ctx) == 0 and _same(_state(g), before)          # nothing pending
+    h = torch.from_numpy(orc.synth_grad(SEED, 1, 1, 0, P)).cuda()
+    assert g.asp_push(1, h, 1) == 0                                          # staleness 0: deferred in the window
+    mid = _state(g)
+    assert ss.lib.ss_flush(g.ctx) == 0 and _same(_state(g), mid)             # issued, state unchanged
+    assert o.asp_push(1, orc.synth_grad(SEED, 1, 1, 0, P), 1)[0] == 0
+    g.sync()
+    assert np.array_equal(g.params(), o.params())
+    import ctypes
+    out = ctypes.c_void_p()
+    assert ss.lib.ss_grad_buffer(g.ctx, 0, ctypes.byref(out)) == SS_E_STATE  # single GPU
+    assert ss.lib.ss_grad_buffer(g.ctx, 5, ctypes.byref(out)) == 1            # SS_E_INVAL: worker out of range
+    assert ss.lib.ss_grad_buffer(g.ctx, 0, None) == 1                         # SS_E_INVAL: null output
+    bad = torch.full((P,), float("inf"), device="cuda")
+    g.asp_push(0, bad, 2)
+    g.flush()
+    assert g.sync_status() == 6                                               # SS_E_DIVERGED
+    assert ss.lib.ss_flush(g.ctx) == 6                                        # sticky
     g.close()
