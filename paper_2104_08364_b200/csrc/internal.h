@@ -28,8 +28,6 @@ struct PeerSync {
                                     // contributes are ready at kernel entry: one-kernel pull exchange)
   uint32_t wait_off;
   uint32_t signal_off;              // !=0: the last CTA to finish signals every rank with base + signal_off
-  uint32_t mid_off;                 // !=0 (one-kernel exchange): after phase A the grid's last CTA signals
-                                    // base + mid_off to every rank, and every CTA waits for it from all ranks
   int32_t end_wait;                 // and then waits until every rank has signalled it
   unsigned long long *trace;        // SS_TRACE: CTA 0 / the last CTA record globaltimer into trace[0..3] (or null)
 };
@@ -81,16 +79,6 @@ struct AspEvent {
   int32_t src0;       // BSP: its gradients are bsp_src[src0 .. src0 + n_src), ascending worker order
   int32_t n_src;
 };
-// Phase A of a one-kernel fused exchange (the scatter_kernel's work inside the window kernel): every hosted push's
-// owner slices -> the owners' inbox slots.
-struct ScatterPhase {
-  const float *src[kMaxEvents];   // full-length hosted gradients
-  int32_t slot[kMaxEvents];       // their inbox slots (window event index)
-  int32_t n_src;
-  float *inbox[kMaxPeers];        // every rank's inbox (this exchange's buffer)
-  int64_t reg_len;
-  int64_t P;
-};
 struct AspArgs {
   AspEvent ev[kMaxEvents];
   const float *bsp_src[kMaxBspSrc];
@@ -105,7 +93,6 @@ struct AspArgs {
   float lam;
   int32_t nesterov;   // as BspArgs::nesterov
   PeerSync sync;
-  ScatterPhase xa;    // used when sync.mid_off != 0
 };
 
 // scatter (fused path): copy every source's owner slices into the owners' inbox slots with posted NVLink stores:

@@ -84,11 +84,11 @@ __device__ void peer_wait(const PeerSync &s, uint32_t epoch) {
 
 // Absolute epochs of this launch: the rank's device counter (advanced by the previous fused kernel) + the offsets.
 struct Ep {
-  uint32_t wait, signal, mid;
+  uint32_t wait, signal;
 };
 __device__ __forceinline__ Ep peer_epochs(const PeerSync &s) {
   const uint32_t b = s.epoch_base ? *reinterpret_cast<const volatile uint32_t *>(s.epoch_base) : 0u;
-  return Ep{b + s.wait_off, s.signal_off ? b + s.signal_off : 0u, s.mid_off ? b + s.mid_off : 0u};
+  return Ep{b + s.wait_off, s.signal_off ? b + s.signal_off : 0u};
 }
 
 // Block-wide, at kernel entry: CTA 0 stamps trace[0]; every CTA waits for the wait epoch when set (CTA 0 stamps
@@ -129,24 +129,6 @@ __device__ void peer_done(const PeerSync &s, const Ep &ep) {
     peer_wait(s, ep.signal);
     trace_mark(s, 3);
   }
-}
-
-// Block-wide, between the two phases of a one-kernel exchange: the grid's last CTA to finish phase A publishes the mid
-// epoch to every rank (after a system-scope fence ordering all of this grid's phase-A stores), then every CTA waits for
-// it from all ranks. The grid must be co-resident (the launcher sizes it to one wave). The CTA counter returns to 0
-// before the signal, so the end-of-kernel count (peer_done) starts afresh.
-__device__ void peer_mid(const PeerSync &s, uint32_t epoch) {
-  __threadfence_system();
-  __syncthreads();
-  __shared__ uint32_t last_mid;
-  if (threadIdx.x == 0) last_mid = atomicAdd(s.ctr, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (last_mid && threadIdx.x == 0) {
-    *s.ctr = 0;
-    __threadfence_system();
-    for (int q = 0; q < s.world; ++q) st_release_sys(s.sig_peer[q] + s.rank, epoch);
-  }
-  peer_wait(s, epoch);
 }
 
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
@@ -373,38 +355,6 @@ __global__ void __launch_bounds__(kThreads) asp_replay_scalar_kernel(const __gri
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// Phase A of the fused exchange: every source's owner slices -> the owners' inbox slots with posted 128-bit NVLink
-// stores (the local slice is read in place by the owner, never copied).
-__device__ __forceinline__ void scatter_phase(const float *const *srcs, const int32_t *slots, int n_src,
-                                              float *const *inbox, int64_t reg_len, int64_t P, int me, int G) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  constexpr int U = 8;  // stores in flight per thread (posted NVLink writes; the loads come from local HBM)
-  for (int k = 0; k < n_src; ++k) {
-    // one contiguous segment per (source, destination rank), no per-element division; destinations in rotated order
-    // (me+1, me+2, ...) so that at any moment the ranks write to distinct receivers instead of all hitting one ingress
-    for (int step = 1; step < G; ++step) {
-      const int r = (me + step) % G;
-      const int64_t lo = min((int64_t)r * reg_len, P), cnt = min((int64_t)(r + 1) * reg_len, P) - lo;
-      const float *src = srcs[k] + lo;
-      float *dst = inbox[r] + (int64_t)slots[k] * reg_len;
-      const int64_t n4 = cnt >> 2;
-      for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
-        float4 x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (q0 + u * stride < n4) x[u] = ld4(src + 4 * (q0 + u * stride));
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = x[u];
-      }
-      const int64_t i = 4 * n4 + tid;  // scalar tail
-      if (i < cnt) dst[i] = src[i];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------------------------
 // K2, TMA form: the same replay, with every push's gradient tile staged through a shared-memory ring filled by 1-D
 // bulk copies (cp.async.bulk, completion on an mbarrier). One CTA walks its tiles (kTmaTile floats = 8 KB); the w and
 // v of a tile live in registers for the whole window; thread 0 keeps kTmaStages tile loads in flight ahead of the
@@ -457,9 +407,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // so every CTA issues all its bulk copies at once and never waits on a CTA barrier.
 // Window events: push (one staged gradient tile), BSP superstep (n_src staged tiles summed in ascending worker order
 // into a register accumulator, then the mean and the momentum update), pull (store of the current w).
-// kExchange: the one-kernel fused exchange — the window's scatter (phase A) runs first in the same grid, then a
-// cross-GPU mid barrier (a separate instantiation: the scatter loop costs registers the other forms do not pay).
-template <bool kRefill, bool kExchange = false>
+template <bool kRefill>
 __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_constant__ AspArgs a) {
   pdl_trigger();
   extern __shared__ __align__(128) float ring[];
@@ -523,13 +471,9 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   }
   pdl_wait();                                                // from here on: data of earlier kernels
   const Ep ep = peer_enter(a.sync);
-  if (kExchange && ep.mid) {                                 // one-kernel exchange: phase A, then the mid barrier
-    scatter_phase(a.xa.src, a.xa.slot, a.xa.n_src, a.xa.inbox, a.xa.reg_len, a.xa.P, a.sync.rank, a.sync.world);
-    peer_mid(a.sync, ep.mid);
-  }
   // the bulk copies below (async proxy) may read slices peers wrote before the flag this CTA acquired (generic
   // proxy): order them after the acquire
-  if ((a.sync.has_wait || ep.mid) && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (a.sync.has_wait && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
   if (my_tiles > 0) load_wv(0);
   __syncthreads();
 
@@ -681,7 +625,32 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
   pdl_trigger();
   pdl_wait();
   const Ep ep = peer_enter(a.sync);
-  scatter_phase(a.src, a.slot, a.n_src, a.inbox, a.reg_len, a.P, a.sync.rank, a.sync.world);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int me = a.sync.rank, G = a.sync.world;
+  constexpr int U = 8;  // stores in flight per thread (posted NVLink writes; the loads come from local HBM)
+  for (int k = 0; k < a.n_src; ++k) {
+    // one contiguous segment per (source, destination rank), no per-element division; destinations in rotated order
+    // (me+1, me+2, ...) so that at any moment the ranks write to distinct receivers instead of all hitting one ingress
+    for (int step = 1; step < G; ++step) {
+      const int r = (me + step) % G;
+      const int64_t lo = min((int64_t)r * a.reg_len, a.P), cnt = min((int64_t)(r + 1) * a.reg_len, a.P) - lo;
+      const float *src = a.src[k] + lo;
+      float *dst = a.inbox[r] + (int64_t)a.slot[k] * a.reg_len;
+      const int64_t n4 = cnt >> 2;
+      for (int64_t q0 = tid; q0 < n4; q0 += stride * U) {
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (q0 + u * stride < n4) x[u] = ld4(src + 4 * (q0 + u * stride));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (q0 + u * stride < n4) *reinterpret_cast<float4 *>(dst + 4 * (q0 + u * stride)) = x[u];
+      }
+      const int64_t i = 4 * n4 + tid;  // scalar tail
+      if (i < cnt) dst[i] = src[i];
+    }
+  }
   peer_done(a.sync, ep);
 }
 
@@ -1012,34 +981,13 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
     k<<<grid_for(k, a.count), kThreads, 0, s>>>(a);
     return cudaGetLastError();
   }
-  static const bool attrs = [] {
+  static const int r = [] {    // resident CTAs per SM at the streaming form's shared memory (thread-safe static init)
+    int res = 0;
     cudaFuncSetAttribute(asp_replay_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
     cudaFuncSetAttribute(asp_replay_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
-    cudaFuncSetAttribute(asp_replay_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
-    cudaFuncSetAttribute(asp_replay_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
-    return true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, asp_replay_tma_kernel<true>, kThreads, kTmaSmem);
+    return res > 0 ? res : 1;
   }();
-  (void)attrs;
-  const bool xch = a.sync.mid_off != 0;
-  auto kernel_of = [&](bool refill) {
-    return refill ? (xch ? asp_replay_tma_kernel<true, true> : asp_replay_tma_kernel<true>)
-                  : (xch ? asp_replay_tma_kernel<false, true> : asp_replay_tma_kernel<false>);
-  };
-  // resident CTAs per SM of an instantiation at a dynamic shared-memory size (cached): every launch below stays within
-  // one wave, which the one-kernel exchange's mid barrier requires (all CTAs co-resident)
-  auto resident = [&](bool refill, int64_t smem) -> int {
-    static std::mutex mu;
-    static std::unordered_map<int64_t, int> cache;
-    const int64_t key = smem * 4 + (refill ? 1 : 0) + (xch ? 2 : 0);
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    int res = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, kernel_of(refill), kThreads, (size_t)smem);
-    res = res > 0 ? res : 1;
-    cache[key] = res;
-    return res;
-  };
   const int64_t nvec = (a.count >> 2) << 2;
   AspArgs b = a;
   b.n_item = 0;                  // gradient sources per tile (the kernel lists them in shared memory)
@@ -1053,22 +1001,23 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
       const int64_t t = std::max<int64_t>(32, ((nvec + want - 1) / want + 31) / 32 * 32);
       if (t > kTmaTile) break;
       const int64_t smem = (int64_t)b.n_item * t * 4;
-      if (smem > kTmaSmemMax || per_sm > resident(false, smem)) continue;
+      if (smem > kTmaSmemMax || per_sm * (smem + 5 * 1024) > 228 * 1024) continue;   // + static smem + reserve
       b.tile = (int32_t)t;
       b.stages = b.n_item;
       const int64_t grid = std::max<int64_t>(1, (nvec + t - 1) / t);
-      return launch_pdl(kernel_of(false), grid, (size_t)smem, s, b);
+      return launch_pdl(asp_replay_tma_kernel<false>, grid, (size_t)smem, s, b);
     }
   }
   // streaming form: grid-stride over kTmaTile tiles, at most one wave of resident CTAs, a kTmaStages-tile ring
+  const int64_t slots = (int64_t)r * num_sms();
   const int64_t tile = kTmaTile;
   const int64_t tiles = (nvec + tile - 1) / tile;
-  const int64_t slots = (int64_t)std::min(resident(true, kTmaSmem), resident(false, kTmaSmem)) * num_sms();
   const int64_t grid = std::max<int64_t>(1, std::min(tiles, slots));
   b.tile = (int32_t)tile;
   b.stages = kTmaStages;
   const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
-  return launch_pdl(kernel_of(items > kTmaStages), grid, kTmaSmem, s, b);
+  if (items > kTmaStages) return launch_pdl(asp_replay_tma_kernel<true>, grid, kTmaSmem, s, b);
+  return launch_pdl(asp_replay_tma_kernel<false>, grid, kTmaSmem, s, b);
 }
 
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {

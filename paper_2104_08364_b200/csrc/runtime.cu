@@ -635,8 +635,7 @@ ss_status flush_fused(ss_ctx *c) {
     const Ev &e = c->win[k];
     if (e.kind == 0 && host_of(c, e.worker) == me) src.push_back({e.src, (int32_t)k});
   }
-  for (const auto &x : src)
-    if (!aligned16(x.first)) return fail(c, SS_E_INVAL, "fused path needs 16-byte aligned gradients");
+  SS_TRY(launch_scatter(c, src, epA));
   ss::AspArgs a;
   std::memset(&a, 0, sizeof a);
   bool vec = true;
@@ -672,30 +671,9 @@ ss_status flush_fused(ss_ctx *c) {
     if (e.kind == 1 && e.data && host_of(c, e.worker) == me &&
         e.dst != c->pbuf + (int64_t)(e.worker - c->first_hosted) * c->P_pad)
       copy_follows = true;
-  double scatter_nv = 0.0;   // NVLink bytes of the window's scatter (phase A)
-  if (vec) {
-    // One kernel for the whole exchange: the window kernel first scatters this rank's pushes into the owners'
-    // inboxes (phase A), passes a cross-GPU mid barrier, then replays the window (phase B): no kernel turnaround
-    // between the phases.
-    a.xa.n_src = (int32_t)src.size();
-    for (size_t k = 0; k < src.size(); ++k) {
-      a.xa.src[k] = src[k].first;
-      a.xa.slot[k] = src[k].second;
-    }
-    for (int32_t q = 0; q < c->world; ++q) a.xa.inbox[q] = c->peer_inbox[q] + inbox_off(c);
-    a.xa.reg_len = c->reg_len;
-    a.xa.P = c->P;
-    for (int32_t q = 0; q < c->world; ++q)
-      if (q != me) scatter_nv += 4.0 * (double)(c->real_hi[q] - c->real_lo[q]) * (double)src.size();
-    const uint32_t base = c->dev_epoch;
-    a.sync = peer_sync(c, 0, epB, end_wait_needed(c, copy_follows), 3);
-    a.sync.mid_off = epA - base;
-  } else {
-    SS_TRY(launch_scatter(c, src, epA));
-    a.sync = peer_sync(c, epA, epB, end_wait_needed(c, copy_follows), 3);
-  }
+  a.sync = peer_sync(c, epA, epB, end_wait_needed(c, copy_follows), 3);
   Timed t;
-  timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull + scatter_nv);
+  timed_begin(c, &t, 1, 4.0 * (double)cnt * (4 + n_push + n_pull), 4.0 * (double)cnt * n_remote_pull);
   SS_CUDA(c, ss::launch_asp_replay(a, vec, c->stream));
   timed_end(c, &t);
   c->xchg += 1;
