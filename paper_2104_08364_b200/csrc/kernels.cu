@@ -926,9 +926,13 @@ int grid_for(K kernel, int64_t work_items) {
 }  // namespace
 
 // Launch with programmatic stream serialization (see pdl_trigger / pdl_wait): only kernels that call pdl_wait before
-// touching global data written by earlier work are launched this way.
+// touching global data written by earlier work are launched this way, and only on one GPU. Kernels of the fused
+// multi-GPU exchange (cross-GPU flag barriers) launch with ordinary serialisation: there PDL measured slower
+// (config 2 at 2 GPUs: 12.3k vs 14.6k steps/s; config 3: 1,192 vs 1,204; profiles/r02_pdl_ab.txt).
+inline bool pdl_for(const PeerSync &p) { return p.world <= 1 && !p.has_wait && p.signal_off == 0; }
+
 template <typename Arg>
-cudaError_t launch_pdl(void (*k)(Arg), int64_t grid, size_t smem, cudaStream_t s, const Arg &arg) {
+cudaError_t launch_pdl(void (*k)(Arg), int64_t grid, size_t smem, cudaStream_t s, const Arg &arg, bool pdl = true) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
@@ -940,8 +944,9 @@ cudaError_t launch_pdl(void (*k)(Arg), int64_t grid, size_t smem, cudaStream_t s
   cfg.attrs = attr;
 #ifdef SS_NO_PDL
   cfg.numAttrs = 0;   // A/B variant (tools/kernel_sweep.py set "pdl"): ordinary stream serialisation
+  (void)pdl;
 #else
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
 #endif
   return cudaLaunchKernelEx(&cfg, k, arg);
 }
@@ -954,12 +959,12 @@ cudaError_t launch_bsp_update(const BspArgs &a, bool vec, cudaStream_t s) {
     if (n4 < (int64_t)resident_ctas(k) * num_sms() * kThreads * kU1) {
       // less than one wave of the streaming form (small P, e.g. config 2): latency-bound, one float4 per thread
       auto ks = bsp_update_kernel<true, 1, 4>;
-      return launch_pdl(ks, grid_for(ks, n4 + 1), 0, s, a);
+      return launch_pdl(ks, grid_for(ks, n4 + 1), 0, s, a, pdl_for(a.sync));
     }
-    return launch_pdl(k, grid_for(k, (n4 + kU1 - 1) / kU1 + 1), 0, s, a);
+    return launch_pdl(k, grid_for(k, (n4 + kU1 - 1) / kU1 + 1), 0, s, a, pdl_for(a.sync));
   }
   auto k = bsp_update_kernel<false>;
-  return launch_pdl(k, grid_for(k, a.count), 0, s, a);
+  return launch_pdl(k, grid_for(k, a.count), 0, s, a, pdl_for(a.sync));
 }
 
 cudaError_t launch_local_sum(const SumArgs &a, bool vec, cudaStream_t s) {
@@ -1005,7 +1010,7 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
       b.tile = (int32_t)t;
       b.stages = b.n_item;
       const int64_t grid = std::max<int64_t>(1, (nvec + t - 1) / t);
-      return launch_pdl(asp_replay_tma_kernel<false>, grid, (size_t)smem, s, b);
+      return launch_pdl(asp_replay_tma_kernel<false>, grid, (size_t)smem, s, b, pdl_for(b.sync));
     }
   }
   // streaming form: grid-stride over kTmaTile tiles, at most one wave of resident CTAs, a kTmaStages-tile ring
@@ -1016,21 +1021,21 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
   b.tile = (int32_t)tile;
   b.stages = kTmaStages;
   const int64_t items = (tiles + grid - 1) / grid * b.n_item;   // most gradient tiles any CTA stages
-  if (items > kTmaStages) return launch_pdl(asp_replay_tma_kernel<true>, grid, kTmaSmem, s, b);
-  return launch_pdl(asp_replay_tma_kernel<false>, grid, kTmaSmem, s, b);
+  if (items > kTmaStages) return launch_pdl(asp_replay_tma_kernel<true>, grid, kTmaSmem, s, b, pdl_for(b.sync));
+  return launch_pdl(asp_replay_tma_kernel<false>, grid, kTmaSmem, s, b, pdl_for(b.sync));
 }
 
 cudaError_t launch_scatter_sum(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_sum_kernel;
   const int G = a.sync.world > 0 ? a.sync.world : 1;
   const int grid = (std::max(grid_for(k, (a.P / 4 + kScsU - 1) / kScsU + 1), G) + G - 1) / G * G;   // whole cycles
-  return launch_pdl(k, grid, 0, s, a);
+  return launch_pdl(k, grid, 0, s, a, false);
 }
 
 cudaError_t launch_scatter(const ScatterArgs &a, cudaStream_t s) {
   auto k = scatter_kernel;
   const int64_t work = a.n_src > 0 ? (a.P / 4 + 3) / 4 + 1 : 1;
-  return launch_pdl(k, grid_for(k, work), 0, s, a);
+  return launch_pdl(k, grid_for(k, work), 0, s, a, false);
 }
 
 cudaError_t launch_synth_grad(uint64_t seed, int32_t j, int64_t k, int64_t i0, int64_t count, float *dst,
