@@ -109,6 +109,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def step_floor(world: int, P: int, S: int, n: int, steps_per_s: float, hbm_peak: float) -> dict:
+    """The bench step's floor on this N: the bytes the method must move through the bounding link, at its peak.
+    G > 1: per GPU per direction, the BSP exchange (RS + AG: 2(G-1)/G * 4 P_pad) plus the ASP round (n pushes routed
+    to the owners and n pull snapshots routed back, n/G of each per GPU: 2 (n/G)(G-1)/G * 4 P_pad), over 900 GB/s
+    NVLink; G = 1: the two kernels' HBM bytes ((n + 4) 4P for the superstep, (2n + 4) 4P for the ASP round) over the
+    measured copy rate."""
+    if world > 1:
+        P_pad = S * (((P + S - 1) // S + 31) // 32 * 32)
+        nv_bytes = 2 * (world - 1) / world * 4 * P_pad * (1 + n / world)
+        floor = {"bound": "nvlink", "bytes_per_gpu_per_direction": nv_bytes, "peak_GBps": 900.0,
+                 "steps_per_s_at_peak": 900e9 / nv_bytes}
+    else:
+        step_bytes = (3 * n + 8) * 4 * P
+        floor = {"bound": "hbm", "bytes": step_bytes, "peak_GBps": hbm_peak,
+                 "steps_per_s_at_peak": hbm_peak * 1e9 / step_bytes}
+    floor["frac_of_floor"] = steps_per_s / floor["steps_per_s_at_peak"]
+    return floor
+
+
 def ncu_traffic(kernel: str, config: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -504,19 +523,7 @@ def run_ours(args):
         phases["bsp_nvlink_frac_of_770_measured"] = phases["bsp_nvlink_busbw_GBps"] / 770.0
         rates["bsp_nvlink_busbw_GBps"] = per_dir / (bsp_only_ms / nr / 1e3) / 1e9
         rates["bsp_nvlink_frac_of_900"] = rates["bsp_nvlink_busbw_GBps"] / 900.0
-    # the step's floor on this N: the bytes the method must move through the bounding link, at its peak.
-    # G > 1: per GPU per direction, the BSP exchange (RS + AG: 2(G-1)/G * 4 P_pad) plus the ASP round (n pushes routed
-    # to the owners and n pull snapshots routed back, n/G of each per GPU: 2 (n/G)(G-1)/G * 4 P_pad), over 900 GB/s
-    # NVLink; G = 1: the two kernels' HBM bytes over the measured copy rate.
-    if world > 1:
-        P_pad = S * (((P + S - 1) // S + 31) // 32 * 32)
-        nv_bytes = 2 * (world - 1) / world * 4 * P_pad * (1 + n / world)
-        floor = {"bound": "nvlink", "bytes_per_gpu_per_direction": nv_bytes, "peak_GBps": 900.0,
-                 "steps_per_s_at_peak": 900e9 / nv_bytes}
-    else:
-        floor = {"bound": "hbm", "bytes": step_bytes, "peak_GBps": hbm_peak,
-                 "steps_per_s_at_peak": hbm_peak * 1e9 / step_bytes}
-    floor["frac_of_floor"] = steps_per_s / floor["steps_per_s_at_peak"]
+    floor = step_floor(world, P, S, n, steps_per_s, hbm_peak)
     line = {
         "metric": METRIC, "value": round(steps_per_s, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

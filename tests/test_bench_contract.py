@@ -57,3 +57,22 @@ def test_multi_gpu_self_launch_command(monkeypatch):
     assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
     assert "--master-addr=127.0.0.1" in cmd and cmd[-6:] == ["--gpus", "4", "--steps", "20", "--warmup", "5"]
     assert cmd[-7].endswith("bench.py")
+
+
+def test_step_floor_values():
+    """The per-N floor the bench line reports next to its value (SURVEY §8(d) bytes per unit), against hand values:
+    config 3 (P = 25,557,032, S = n = 8; P_pad = 25,557,248) at G = 2: 2 * 1/2 * 4 * P_pad * (1 + 8/2) = 511.1 MB per
+    GPU per direction -> 1,760.8 steps/s at 900 GB/s; at G = 4: 2 * 3/4 * 4 * P_pad * 3 = 460.0 MB -> 1,956.4; one GPU:
+    (3 * 8 + 8) * 4 * P = 3.271 GB at 6,543.1 GB/s -> 2,000.2 steps/s."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    P, S, n = 25_557_032, 8, 8
+    f2 = bench.step_floor(2, P, S, n, 1000.0, 6543.1)
+    assert abs(f2["bytes_per_gpu_per_direction"] - 511_144_960) < 1 and abs(f2["steps_per_s_at_peak"] - 1760.75) < 0.01
+    f4 = bench.step_floor(4, P, S, n, 1000.0, 6543.1)
+    assert abs(f4["bytes_per_gpu_per_direction"] - 460_030_464) < 1 and abs(f4["steps_per_s_at_peak"] - 1956.39) < 0.01
+    f1 = bench.step_floor(1, P, S, n, 1000.0, 6543.1)
+    assert f1["bytes"] == 32 * 4 * P and abs(f1["steps_per_s_at_peak"] - 2000.15) < 0.01
+    assert abs(f1["frac_of_floor"] - 1000.0 / f1["steps_per_s_at_peak"]) < 1e-12
