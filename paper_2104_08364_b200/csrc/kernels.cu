@@ -413,6 +413,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ const float *item_src[kMaxItems];
+  struct SEv {                                               // the window's events, copied once per CTA: the event
+    float *dst;                                              // loop reads shared memory instead of indexing the
+    float lr, mu, divisor;                                   // kernel parameters at a run-time index
+    int32_t kind, n_src;
+  };
+  __shared__ SEv sev[kMaxEvents];
   // ring depth and tile length: compile-time in the streaming (refill) form, per launch in the small-launch form
   const int n_stage = kRefill ? kTmaStages : a.stages;      // (<= kMaxStages)
   const float lam = a.lam;
@@ -466,6 +472,9 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
     };
     list(lane, s0 - c0, c0);
     list(lane + 32, tot0 + s1 - c1, c1);
+    if (kRefill)   // (streaming form: config 3 asp_replay 333 -> 327 us; the short small-launch form loses more in the copy)
+      for (int e = lane; e < a.n_ev; e += 32)
+        sev[e] = SEv{a.ev[e].dst, a.ev[e].lr, a.ev[e].mu, a.ev[e].divisor, a.ev[e].kind, a.ev[e].n_src};
     for (int st = lane; st < n_stage; st += 32) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -530,10 +539,12 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
   for (int64_t tl = 0; tl < my_tiles; ++tl) {
     const int64_t off = (blockIdx.x + tl * gridDim.x) * tsz;
     for (int e = 0; e < a.n_ev; ++e) {
-      const int kind = a.ev[e].kind;
+      // event fields: the shared copy in the streaming form, the kernel parameters (read only where used) otherwise
+#define EVF(f) (kRefill ? sev[e].f : a.ev[e].f)
+      const int kind = EVF(kind);
       if (kind == 0) {
         wait_item();
-        const float neg_eta = -a.ev[e].lr, mu = a.ev[e].mu;
+        const float neg_eta = -EVF(lr), mu = EVF(mu);
 #pragma unroll
         for (int u = 0; u < kTU; ++u) {
           if (!ok[u]) continue;
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
         release();
       } else if (kind == 2) {
         float4 acc[kTU];
-        const int ns = a.ev[e].n_src;
+        const int ns = EVF(n_src);
         for (int k = 0; k < ns; ++k) {
           wait_item();
 #pragma unroll
@@ -561,8 +572,8 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
           }
           release();
         }
-        const float dv = a.ev[e].divisor;
-        const Upd up{dv, 1.0f / dv, a.ev[e].mu, -a.ev[e].lr, lam, is_pow2(dv), nest};
+        const float dv = EVF(divisor);
+        const Upd up{dv, 1.0f / dv, EVF(mu), -EVF(lr), lam, is_pow2(dv), nest};
 #pragma unroll
         for (int u = 0; u < kTU; ++u) {
           if (!ok[u]) continue;
@@ -571,12 +582,14 @@ __global__ void __launch_bounds__(kThreads) asp_replay_tma_kernel(const __grid_c
           up(acc[u].z, wv[u].z, vv[u].z);
           up(acc[u].w, wv[u].w, vv[u].w);
         }
-      } else if (a.ev[e].dst != nullptr) {
+      } else if (EVF(dst) != nullptr) {
+        float *const dst = EVF(dst);
 #pragma unroll
         for (int u = 0; u < kTU; ++u)
-          if (ok[u]) st4(a.ev[e].dst + off + 4 * (threadIdx.x + u * kThreads), wv[u]);
+          if (ok[u]) st4(dst + off + 4 * (threadIdx.x + u * kThreads), wv[u]);
       }
     }
+#undef EVF
 #pragma unroll
     for (int u = 0; u < kTU; ++u) {
       if (!ok[u]) continue;
@@ -1006,7 +1019,7 @@ cudaError_t launch_asp_replay(const AspArgs &a, bool vec, cudaStream_t s) {
       const int64_t t = std::max<int64_t>(32, ((nvec + want - 1) / want + 31) / 32 * 32);
       if (t > kTmaTile) break;
       const int64_t smem = (int64_t)b.n_item * t * 4;
-      if (smem > kTmaSmemMax || per_sm * (smem + 5 * 1024) > 228 * 1024) continue;   // + static smem + reserve
+      if (smem > kTmaSmemMax || per_sm * (smem + 7 * 1024) > 228 * 1024) continue;   // + static smem + reserve
       b.tile = (int32_t)t;
       b.stages = b.n_item;
       const int64_t grid = std::max<int64_t>(1, (nvec + t - 1) / t);
