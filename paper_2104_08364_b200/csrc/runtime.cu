@@ -732,7 +732,10 @@ ss_status flush(ss_ctx *c) {
   }
 
   if (cnt > 0) {
-    if (c->world == 1 && c->win.size() == 1 && c->win[0].kind == 2) {
+    // A lone superstep of a large vector runs in bsp_update (config 3: 0.977 vs 0.918 of HBM through the window
+    // kernel); below 2^20 parameters the window kernel's small-launch form is the faster one (config 2: 63.7k vs
+    // 61.5k steps/s eager, profiles/r02_lone_superstep_ab.txt)
+    if (c->world == 1 && c->win.size() == 1 && c->win[0].kind == 2 && c->P > (int64_t)1 << 20) {
       // a lone superstep (flushed at its data dependency): the streaming aggregate-and-update kernel, which reads
       // each gradient once and w, v once — the same arithmetic as the window kernel's BSP event
       const Ev &e = c->win[0];
