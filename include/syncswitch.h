@@ -113,7 +113,8 @@ ss_status ss_get_exchange(ss_ctx *ctx, int32_t *mode, int32_t *nvls);
  * first use. Errors: SS_E_INVAL (worker not hosted here), SS_E_STATE (single GPU or NCCL mode). */
 ss_status ss_pull_buffer(ss_ctx *ctx, int32_t worker, float **out);
 
-/* Fused multi-GPU mode: the CUDA-IPC-mapped gradient buffer (device fp32[P_pad], owned by the context, valid until
+/* P:1072 ("push the computed gradients to all PSs"), SV §8(f) NEXT-1 (the owner loads the peers' gradient slices).
+ * Fused multi-GPU mode: the CUDA-IPC-mapped gradient buffer (device fp32[P_pad], owned by the context, valid until
  * ss_destroy; the padding past n_params must stay 0) of a worker hosted on this rank. In mode 3 owners load their
  * region of it over NVLink during a superstep: a worker that writes its gradient here and passes this pointer to
  * ss_bsp_step saves the copy-in. Like every gradient it is BORROWED by the superstep until ss_sync. Collective on
@@ -227,7 +228,9 @@ ss_status ss_asp_replay(ss_ctx *ctx, const ss_event *ev, int64_t n_ev, int64_t *
  * including a fused-path cross-GPU wait that timed out). Not allowed while capturing a graph (SS_E_STATE). */
 ss_status ss_sync(ss_ctx *ctx);
 
-/* Issue the device work of the calls accepted so far (the pending window, including one-GPU supersteps deferred into
+/* SV §8b ("device data movement is stream-ordered and may be lazily batched"); P:1072 (a worker computes its next
+ * gradient from the parameters it pulled).
+ * Issue the device work of the calls accepted so far (the pending window, including one-GPU supersteps deferred into
  * it) on the context's stream, without waiting. A caller whose next inputs depend on these results (a worker that
  * computes its next gradient from a pulled snapshot, or from the parameters after a superstep) flushes, then orders
  * its own stream after the context's (ss_wait_stream) — the window batching never reaches across such a dependency.
