@@ -138,6 +138,7 @@ struct ss_ctx {
   int64_t cap_v0 = 0, cap_dv = 0, cap_log0 = 0, cap_rel_since = 0;
   uint64_t cap_ddropped = 0;
   uint32_t cap_epoch0 = 0, cap_depoch = 0;   // fused-path flag epochs consumed by the captured step
+  int64_t cap_xchg0 = 0;                     // fused exchanges issued before the capture
   std::vector<int64_t> cap_base0, cap_log;   // log records appended during the captured step
   // instrumentation
   unsigned long long *trace_dev = nullptr;   // SS_TRACE=<prefix>: 4 globaltimer stamps per fused launch
@@ -583,10 +584,13 @@ int64_t inbox_off(const ss_ctx *c) {
 
 // Does a phase-B kernel have to wait, at its end, until every rank finished its phase B? Only when something after
 // it on this rank's stream depends on the peers' stores being complete (a hosted pull copied out of its pull buffer),
-// when the inbox is single-buffered (the next phase A would overwrite slices still being read), or while capturing
-// (a graph replays its buffer choice, so keep the barrier).
+// or when the inbox is single-buffered (the next phase A would overwrite slices still being read). With two buffers,
+// exchange x's phase A on one rank starts only after that rank's phase B of x-1 saw every rank's phase A of x-1 —
+// which each rank issued after finishing its phase B of x-2, the last reader of the buffer x reuses. A captured
+// graph bakes its exchanges' buffers in: an even number per capture keeps the alternation across replays, an odd
+// number gets a closing barrier (ss_capture_end).
 bool end_wait_needed(const ss_ctx *c, bool copy_follows) {
-  return copy_follows || c->inbox_bufs == 1 || c->capturing || c->nvls.ready;
+  return copy_follows || c->inbox_bufs == 1 || c->nvls.ready;
 }
 
 // Phase A of every fused exchange: hosted sources' owner slices -> owners' inbox slots, then signal `epoch`.
@@ -1519,6 +1523,7 @@ ss_status ss_capture_begin(ss_ctx *c) {
   c->cap_ddropped = c->dropped;
   c->cap_rel_since = c->version - c->asp_since;
   c->cap_epoch0 = c->epoch;
+  c->cap_xchg0 = c->xchg;
   SS_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   c->capturing = true;
   return SS_OK;
@@ -1527,6 +1532,18 @@ ss_status ss_capture_begin(ss_ctx *c) {
 ss_status ss_capture_end(ss_ctx *c, int64_t *version_delta) {
   if (!c || !c->capturing) return c ? fail(c, SS_E_STATE, "not capturing") : SS_E_INVAL;
   ss_status fl = flush(c);   // every queued window joins the graph
+  if (fl == SS_OK && c->world > 1 && c->fused_mode != 0 && c->inbox_bufs == 2 && ((c->xchg - c->cap_xchg0) & 1)) {
+    // an odd number of fused exchanges: consecutive replays would reuse one inbox buffer back to back, so the graph
+    // closes with a cross-GPU barrier (an empty scatter launch that signals and waits for every rank)
+    ss::ScatterArgs b;
+    std::memset(&b, 0, sizeof b);
+    for (int32_t q = 0; q < c->world; ++q) b.inbox[q] = c->peer_inbox[q];
+    b.reg_len = c->reg_len;
+    b.P = c->P;
+    b.sync = peer_sync(c, 0, ++c->epoch, true, 0);
+    cudaError_t le = ss::launch_scatter(b, c->stream);
+    if (le != cudaSuccess) fl = fail(c, SS_E_CUDA, "capture barrier: %s", cudaGetErrorString(le));
+  }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(c->stream, &g);
   c->capturing = false;

@@ -267,6 +267,32 @@ def test_multi_gpu_graph_capture(orc, world, fused):
 
 
 @pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fused", [1, 2, 3])
+def test_multi_gpu_graph_capture_odd_exchanges(orc, world, fused):
+    """A captured step holding ONE fused exchange (a BSP superstep): consecutive replays would reuse one inbox buffer,
+    so the capture closes with a cross-GPU barrier (ss_capture_end). Eight replays equal ten supersteps of the
+    oracle, bit-exact in the exact modes."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    P, n, S, R = 464_154, 8, 8, 8
+    with tempfile.TemporaryDirectory() as tmp:
+        launch(world, ["--P", P, "--nworkers", n, "--nshards", S, "--window", 2 * n, "--fused", fused,
+                       "--capture", R, "--capture-bsp-only", 1], tmp)
+        res = [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
+    w0 = orc.synth_grad(SEED + 1, 255, 0, 0, P) * np.float32(64.0)
+    o = orc.Oracle(w0, S, n, 0.1, 0.9)
+    o.set_lr_schedule([1 << 40], [0.5])
+    bsp_h = [orc.synth_grad(SEED, j, 0, 0, P) for j in range(n)]
+    for _ in range(R + 2):
+        assert o.bsp_step(bsp_h, versions=[o.version] * n) == 0
+    cmp = np.array_equal if fused in (1, 3) else close_c13
+    for r in res:
+        assert int(r["version"]) == o.version == R + 2
+        assert np.array_equal(r["log"], o.log()) and np.array_equal(r["hist"], o.stats(64)["hist"])
+        assert cmp(r["w"], o.params()) and cmp(r["v"], o.velocity())
+
+
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("fused", [0, 1, 3])
 def test_multi_gpu_host_buffers(orc, world, fused):
     """The e2e path at G > 1: gradients and pull destinations in pinned host memory (staged by the library) —
