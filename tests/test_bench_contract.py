@@ -26,14 +26,21 @@ def test_reference_arm_json_line():
 
 
 def test_gpu_line_recorded_with_required_keys():
-    with open(os.path.join(ROOT, "profiles", "r01_bench_config3.json")) as f:
+    """The committed round-2 default line (config 3, 1 GPU) carries every key the contract names, and its numbers are
+    internally consistent: roofline fraction = achieved / peak, the dominant kernel's time within a step, the step's
+    floor fraction = value / floor."""
+    with open(os.path.join(ROOT, "profiles", "r02_bench_config3.json")) as f:
         d = json.loads(f.read().splitlines()[0])
-    for k in ("roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+    for k in ("roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks", "step_floor", "protocol_rates"):
         assert k in d, k
     rf = d["roofline"]
     assert set(rf) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
+    assert rf["avg_launch_us"] < 1e3 * d["ms_per_step"]
     assert d["gpu_launches"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    fl = d["step_floor"]
+    assert abs(fl["frac_of_floor"] - d["value"] / fl["steps_per_s_at_peak"]) < 1e-6 and fl["frac_of_floor"] <= 1.0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
 
 
 def test_multi_gpu_self_launch_command(monkeypatch):
