@@ -1210,12 +1210,12 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
   bool vec = true;
   int32_t k = 0;
   std::vector<int32_t> ids;             // hosted members, ascending
-  const bool pull = c->world > 1 && c->fused_mode == 3;
+  const bool pull_mode = c->world > 1 && c->fused_mode == 3;
   for (int32_t j = 0; j < c->n; ++j) {  // ascending worker order (reading C12)
     if (!by[j]) continue;
     ids.push_back(j);
     const float *g = by[j];
-    if (!pull) SS_TRY(resolve_src(c, by[j], &g));   // (pull mode copies straight into its gradient buffers)
+    if (!pull_mode) SS_TRY(resolve_src(c, by[j], &g));   // (mode 3 copies straight into its gradient buffers)
     a.g[k++] = g;
     vec = vec && aligned16(g);
   }
@@ -1235,7 +1235,7 @@ ss_status ss_bsp_step(ss_ctx *c, const float *const *grads, const int32_t *worke
     timed_begin(c, &t, 0, 4.0 * (double)c->P * (k + 4));
     SS_CUDA(c, ss::launch_bsp_update(a, vec, c->stream));
     timed_end(c, &t);
-  } else if (pull) {
+  } else if (pull_mode) {
     // Fused pull exchange (SURVEY §8(f) NEXT-1 as one kernel, "push the computed gradients to all PSs"): every
     // rank's hosted gradients sit in its exported gradient buffers (ss_grad_buffer hands them out: zero copy; any other
     // buffer is copied in on the stream first). Each owner loads the members' slices of its region — hosted ones from

@@ -3,7 +3,8 @@
 
     python tools/kernel_sweep.py build <set>            # here: tools/variants/<set>_<tag>.so
     python tools/kernel_sweep.py run <set> [--config 3] # on the GPU: bench.py per variant
-Sets: replay (asp_replay_tma_kernel tile x stages; profiles/r01_replay_sweep.txt), bsp (bsp_update float4 per thread x gradients loaded together).
+Sets: replay (asp_replay_tma_kernel tile x stages; profiles/r01_replay_sweep.txt, r02_replay_sweep.txt), bsp (bsp_update
+float4 per thread x gradients loaded together), pdl (programmatic dependent launch off; profiles/r02_pdl_ab.txt).
 """
 import json
 import os
@@ -15,7 +16,6 @@ OUT = os.path.join(ROOT, "tools", "variants")
 SETS = {
     "replay": [{"SS_TMA_TILE": t, "SS_TMA_STAGES": s} for t, s in
                [(2048, 6), (2048, 10), (2048, 12), (2048, 14), (2048, 16), (1024, 20), (4096, 6)]],
-    "balance": [{"SS_TMA_BALANCE": b, "SS_TMA_STAGES": st} for b, st in [(0, 10), (1, 10), (0, 12), (1, 12)]],
     "bsp": [{"SS_BSP_U": u, "SS_BSP_G": g} for u, g in [(2, 8), (1, 8), (1, 4), (2, 4), (4, 4), (4, 2), (3, 8)]],
     "pdl": [{"SS_NO_PDL": 1}],   # programmatic dependent launch off (A/B against the default library)
 }
