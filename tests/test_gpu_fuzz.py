@@ -142,7 +142,7 @@ def _single(ss, orc, case_seed):
     o.close()
 
 
-@pytest.mark.parametrize("case_seed", list(range(64)))
+@pytest.mark.parametrize("case_seed", list(range(int(os.environ.get("SS_FUZZ_CASES", "64")))))
 def test_random_protocol_sequences_bit_exact(ss, orc, case_seed):
     _single(ss, orc, 1000 + case_seed)
 
@@ -154,7 +154,7 @@ def close_c13(x, y, rel=1e-5):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case_seed", list(range(8)))
+@pytest.mark.parametrize("case_seed", list(range(int(os.environ.get("SS_FUZZ_MULTI_CASES", "8")))))
 def test_random_protocol_sequences_multi_gpu(orc, world, case_seed):
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
